@@ -1,0 +1,206 @@
+"""Oracle request flow (TEST INFRASTRUCTURE ONLY — see oracle/__init__.py).
+
+The request flow of Alg. 1, for batches that are admitted
+whole (C1/C2/C3/C5: the pool is sized so they fit).  For one batch:
+
+ 1. match_prefix every request in list order (Alg. 1 "for req in requests",
+    P:526-528); the usable prefix is capped at n-1 (R11) so every request has
+    a query row;
+ 2. increase_ref_counter on every matched node;
+ 3. alloc(sum of new tokens); on failure evict the shortfall and retry once
+    (R6); request i takes the next n_i - m_i slots (R8);
+ 4. extend attention for all new tokens (B.run);
+ 5. decode steps: every still-running request allocates one slot per step
+    (evict-retry as above), stores its newest token's KV and attends;
+ 6. a request that produced its last token finishes: decrease_ref_counter
+    then insert(prompt + outputs, slots), in batch order.
+
+Generated tokens come from the mock model in rxgen (next_token of the prefix
+hash), so both sides see the same token streams.  The KV written to a slot is
+identified by the prefix hash of the token it belongs to (rxgen.values); the
+oracle's pool stores that hash per slot and expands values on read.
+
+Every tree result is appended to ``trace`` as a plain tuple; slot lists are
+kept whole.  tests/ compare this trace with the library's, element by element.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from rxgen.hashing import prefix_hashes, next_token, splitmix64_int, MASK64
+from rxgen.values import gen_values, KIND_K, KIND_V, KIND_Q
+
+from .radix import RadixCache
+from . import attention
+
+
+class OOM(Exception):
+    pass
+
+
+class Seq:
+    """One request while it runs: tokens so far, their hashes, their slots."""
+
+    def __init__(self, rid, prompt, n_out, seed, vocab):
+        self.rid = rid
+        self.tokens = [int(t) for t in prompt]
+        self.hashes = [int(h) for h in prefix_hashes(self.tokens, seed)]
+        self.n_prompt = len(self.tokens)
+        self.n_out = n_out
+        self.vocab = vocab
+        self.slots = []
+        self.node = None
+        self.prefix_len = 0
+
+    def gen_next(self):
+        """Mock model: append the token generated after the current last position."""
+        h = self.hashes[-1]
+        t = next_token(h, self.vocab)
+        self.tokens.append(t)
+        self.hashes.append(splitmix64_int((h ^ t) & MASK64))
+
+
+class OracleEngine:
+    def __init__(self, wl, sample_extend=None, sample_decode=None, q_scale=1.0):
+        """sample_extend(call_idx, B, prefix_lens, extend_lens) -> list of (req_idx, j) rows to evaluate, or None (= none);
+        sample_decode(call_idx, step, B) -> list of req_idx to evaluate."""
+        self.wl = wl
+        self.shape = wl.shape
+        self.tree = RadixCache(wl.num_slots)
+        self.slot_hash = {}
+        self.trace = []
+        self.sample_extend = sample_extend
+        self.sample_decode = sample_decode
+        self.q_scale = q_scale
+        self.extend_calls = 0
+        self.decode_calls = 0
+        self.outputs = {}           # ("extend", call, req_idx, j) / ("decode", call, req_idx) -> float64 [H_q, hd]
+        self.stats = {"prompt_tokens": 0, "cached_prompt_tokens": 0}
+
+    # ------------------------------------------------------------ pool / values
+    def _kv(self, slots, g, kind):
+        hs = np.array([self.slot_hash[int(s)] for s in slots], dtype=np.uint64)
+        return gen_values(hs, [g], kind, self.shape.head_dim)[:, 0].float().numpy().astype(np.float64)
+
+    def _q(self, h, heads):
+        return gen_values(np.array([h], dtype=np.uint64), heads, KIND_Q, self.shape.head_dim,
+                          scale=self.q_scale)[0].float().numpy().astype(np.float64)
+
+    def _attend(self, seq: Seq, p: int):
+        """o[H_q, hd] for the query at absolute position p of seq, read through the pool by slot."""
+        sh = self.shape
+        G = sh.group
+        out = np.zeros((sh.h_q, sh.head_dim))
+        slots = seq.slots[:p + 1]
+        for g in range(sh.h_kv):
+            kmat = self._kv(slots, g, KIND_K)
+            vmat = self._kv(slots, g, KIND_V)
+            qg = self._q(seq.hashes[p], range(g * G, (g + 1) * G))
+            out[g * G:(g + 1) * G] = attention.attend_row(qg, kmat, vmat, sh.sm_scale)
+        return out
+
+    # ------------------------------------------------------------ tree steps
+    def _alloc(self, n):
+        s = self.tree.alloc(n)
+        if s is None:
+            short = n - self.tree.available()
+            evicted, runs = self.tree.evict(short)
+            self.trace.append(("evict", short, evicted, tuple(tuple(r) for r in runs)))
+            s = self.tree.alloc(n)
+            if s is None:
+                raise OOM(f"need {n}, available {self.tree.available()}")
+        self.trace.append(("alloc", n, tuple(s)))
+        return s
+
+    def _finish(self, seq: Seq):
+        d = self.tree.dec_ref(seq.node)
+        self.trace.append(("dec_ref", seq.rid, d))
+        new_cached, dup = self.tree.insert(seq.tokens, seq.slots)
+        self.trace.append(("insert", seq.rid, new_cached, dup))
+
+    def run_batch(self, reqs, rids=None):
+        """Run one admitted batch to completion; returns the finished Seqs (with full tokens)."""
+        wl = self.wl
+        seqs = []
+        for i, r in enumerate(reqs):
+            rid = rids[i] if rids is not None else r.tag
+            seqs.append(Seq(rid, r.prompt, r.max_new_tokens, wl.seed, wl.vocab))
+        # 1. match_prefix; usable prefix capped at n-1 (R11)
+        for s in seqs:
+            node, m, slots = self.tree.match_prefix(s.tokens)
+            self.trace.append(("match", s.rid, m, tuple(slots)))
+            s.node = node
+            s.prefix_len = min(m, s.n_prompt - 1)
+            s.slots = list(slots[:s.prefix_len])
+            self.stats["prompt_tokens"] += s.n_prompt
+            self.stats["cached_prompt_tokens"] += s.prefix_len
+        # 2. increase_ref_counter
+        for s in seqs:
+            self.trace.append(("inc_ref", s.rid, self.tree.inc_ref(s.node)))
+        # 3. alloc with evict-retry
+        ext = [s.n_prompt - s.prefix_len for s in seqs]
+        new = self._alloc(sum(ext))
+        off = 0
+        for s, n in zip(seqs, ext):
+            s.slots.extend(new[off:off + n])
+            off += n
+        # 4. extend: store new KV (slot -> prefix hash), then attend
+        call = self.extend_calls
+        self.extend_calls += 1
+        for s in seqs:
+            for p in range(s.prefix_len, s.n_prompt):
+                self.slot_hash[s.slots[p]] = s.hashes[p]
+        rows = self.sample_extend(call, seqs) if self.sample_extend else []
+        for (bi, j) in rows:
+            s = seqs[bi]
+            self.outputs[("extend", call, bi, j)] = self._attend(s, s.prefix_len + j)
+        # 5./6. finish requests with no outputs, then decode
+        for s in seqs:
+            if s.n_out == 0:
+                self._finish(s)
+        running = [s for s in seqs if s.n_out > 0]
+        step = 0
+        while running:
+            for s in running:
+                s.gen_next()
+            new = self._alloc(len(running))
+            for s, slot in zip(running, new):
+                s.slots.append(slot)
+                self.slot_hash[slot] = s.hashes[-1]
+            call = self.decode_calls
+            self.decode_calls += 1
+            idx = self.sample_decode(call, step, running) if self.sample_decode else []
+            for bi in idx:
+                s = running[bi]
+                self.outputs[("decode", call, bi)] = self._attend(s, len(s.tokens) - 1)
+            step += 1
+            still = []
+            for s in running:
+                if len(s.tokens) - s.n_prompt >= s.n_out:
+                    self._finish(s)
+                else:
+                    still.append(s)
+            running = still
+        self.trace.append(("sizes", self.tree.evictable_size(), self.tree.total_cached(), self.tree.available()))
+        return seqs
+
+    # ------------------------------------------------------------ workloads
+    def run_workload(self):
+        """Run a whole workload (phases for C1/C2/C5; turns for C3)."""
+        wl = self.wl
+        if wl.name == "C3":
+            return self._run_chat()
+        for kind, reqs in wl.phases:
+            self.run_batch(reqs)
+        return self
+
+    def _run_chat(self):
+        from rxgen.workloads import Request
+        m = self.wl.meta
+        hist = [np.asarray(m["system"], dtype=np.int32) for _ in m["turn_inputs"]]
+        for t in range(m["turns"]):
+            reqs = [Request(np.concatenate([hist[s], m["turn_inputs"][s][t]]), m["turn_outputs"][s][t], f"s{s}t{t}")
+                    for s in range(len(hist))]
+            done = self.run_batch(reqs)
+            hist = [np.asarray(d.tokens, dtype=np.int32) for d in done]
+        return self

@@ -1,0 +1,145 @@
+"""Workload shapes C1-C5 (BASELINE.json "configs") as seeded token streams.
+
+Only inputs live here: attention shapes, pool sizes, and the prompt token
+lists / output lengths of each request.  How requests flow through the radix
+tree and the kernels is the method, and lives in the oracle and in the
+library's harness separately.  Parameters the configs leave open are fixed in
+SURVEY.md §8(d) ("Concrete synthetic inputs"); DESIGN.md restates them.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Shape:
+    h_q: int
+    h_kv: int
+    head_dim: int
+
+    @property
+    def group(self) -> int:
+        return self.h_q // self.h_kv
+
+    @property
+    def sm_scale(self) -> float:
+        # Reading R12: 1/sqrt(head_dim), passed as fp32.
+        return float(np.float32(1.0 / math.sqrt(self.head_dim)))
+
+
+@dataclass
+class Request:
+    """A prompt plus the number of tokens the mock model will generate."""
+    prompt: np.ndarray            # int32 tokens
+    max_new_tokens: int
+    tag: str = ""
+
+
+@dataclass
+class Workload:
+    name: str
+    shape: Shape
+    num_slots: int
+    vocab: int
+    seed: int
+    # phases: list of ("hint", [Request]) / ("batch", [Request]) in order.
+    phases: list = field(default_factory=list)
+    meta: dict = field(default_factory=dict)
+
+
+def _rand_tokens(rng, n, vocab):
+    return rng.integers(1, vocab, size=n, dtype=np.int64).astype(np.int32)
+
+
+def c1(seed: int = 0, n_req: int = 16, prefix: int = 64, new: int = 32, decode: int = 16,
+       num_slots: int = 4096) -> Workload:
+    """C1: 8 q / 2 kv heads, hd 64, 16 requests sharing a 64-token prefix, 32 new each, 16 decode steps."""
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    pre = _rand_tokens(rng, prefix, vocab)
+    reqs = [Request(np.concatenate([pre, _rand_tokens(rng, new, vocab)]), decode, f"r{i}") for i in range(n_req)]
+    return Workload("C1", Shape(8, 2, 64), num_slots, vocab, seed,
+                    [("hint", [Request(pre, 0, "prefix")]), ("batch", reqs)],
+                    {"prefix": prefix, "new": new, "decode": decode})
+
+
+def c2(seed: int = 0, n_req: int = 64, prefix: int = 1536, new_lo: int = 64, new_hi: int = 192,
+       decode: int = 64, num_slots: int = 32768, fixed_new: int | None = None) -> Workload:
+    """C2: Llama-2-7B attention (32/32/128), 5-shot MMLU-like batch 64 sharing a ~1.5k prefix."""
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    pre = _rand_tokens(rng, prefix, vocab)
+    reqs = []
+    for i in range(n_req):
+        n = fixed_new if fixed_new is not None else int(rng.integers(new_lo, new_hi + 1))
+        reqs.append(Request(np.concatenate([pre, _rand_tokens(rng, n, vocab)]), decode, f"q{i}"))
+    return Workload("C2", Shape(32, 32, 128), num_slots, vocab, seed,
+                    [("hint", [Request(pre, 0, "prefix")]), ("batch", reqs)],
+                    {"prefix": prefix, "decode": decode})
+
+
+def c3(seed: int = 0, sessions: int = 256, turns: int = 4, in_lo: int = 256, in_hi: int = 512,
+       out_lo: int = 256, out_hi: int = 512, num_slots: int = 1 << 20, system_prompt: int = 0) -> Workload:
+    """C3: Llama-3-8B GQA (32/8/128) multi-turn chat; turn t prompt = history + new input.
+
+    The per-turn inputs and output lengths are drawn here; the prompt of turn
+    t > 0 depends on the generated answers of turn t-1, which the drivers
+    append themselves (meta["turn_inputs"][s][t], meta["turn_outputs"][s][t]).
+    """
+    rng = np.random.default_rng(seed)
+    vocab = 128256
+    sysp = _rand_tokens(rng, system_prompt, vocab) if system_prompt else np.zeros(0, np.int32)
+    inputs = [[_rand_tokens(rng, int(rng.integers(in_lo, in_hi + 1)), vocab) for _ in range(turns)]
+              for _ in range(sessions)]
+    outs = [[int(rng.integers(out_lo, out_hi + 1)) for _ in range(turns)] for _ in range(sessions)]
+    return Workload("C3", Shape(32, 8, 128), num_slots, vocab, seed, [],
+                    {"turn_inputs": inputs, "turn_outputs": outs, "turns": turns, "system": sysp})
+
+
+def c4(seed: int = 0, root: int = 2048, depth: int = 3, fanout: int = 4, p_lo: int = 32, p_hi: int = 96,
+       t_lo: int = 32, t_hi: int = 64, capacity_frac: float = 0.6) -> Workload:
+    """C4: tree-of-thought, depth 3 x fan-out 4 on a 2k root, pool at 60% of the tree's distinct tokens.
+
+    meta["nodes"][level] = list of (parent_index, branch_prompt_tokens, thought_len).
+    Reading R18 (C4a): capacity = ceil(0.6 * T), T = distinct tokens of the full tree.
+    """
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    rt = _rand_tokens(rng, root, vocab)
+    levels = []
+    prev = 1
+    total = root
+    for lvl in range(depth):
+        nodes = []
+        for parent in range(prev):
+            for _ in range(fanout):
+                bp = _rand_tokens(rng, int(rng.integers(p_lo, p_hi + 1)), vocab)
+                tl = int(rng.integers(t_lo, t_hi + 1))
+                nodes.append((parent, bp, tl))
+                total += len(bp) + tl
+        levels.append(nodes)
+        prev = len(nodes)
+    cap = int(math.ceil(capacity_frac * total)) + 1   # +1: slot 0 is the padding sink
+    return Workload("C4", Shape(32, 32, 128), cap, vocab, seed, [],
+                    {"root": rt, "levels": levels, "distinct_tokens": total})
+
+
+def c5(seed: int = 0, n_req: int = 128, prefix: int = 8192, question: int = 128, decode: int = 32,
+       num_slots: int = 65536, ragged: bool = False) -> Workload:
+    """C5: Llama-2-70B shape (64/8/128) long-prefix RAG: 8k shared context, batch 128."""
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    pre = _rand_tokens(rng, prefix, vocab)
+    reqs = []
+    for i in range(n_req):
+        n = int(rng.integers(64, 257)) if ragged else question
+        reqs.append(Request(np.concatenate([pre, _rand_tokens(rng, n, vocab)]), decode, f"q{i}"))
+    return Workload("C5", Shape(64, 8, 128), num_slots, vocab, seed,
+                    [("hint", [Request(pre, 0, "context")]), ("batch", reqs)],
+                    {"prefix": prefix, "decode": decode})
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
