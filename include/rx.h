@@ -1,0 +1,245 @@
+/*
+ * rx.h — C ABI of the B200-native RadixAttention hot path (arXiv 2312.07104).
+ *
+ * Citations: "P:n" = PAPER.md line n (section in brackets), "S:n" = SPEC.md
+ * line n, "R<k>" = reading k of DESIGN.md "Readings".
+ *
+ * Two halves behind one library (librx.so):
+ *
+ *  1. a host radix tree over a token-slot pool (rx_cache_*, rx_match_prefix,
+ *     rx_insert, rx_inc_ref, rx_dec_ref, rx_evict, rx_alloc, rx_free, ...):
+ *     the paper's "radix tree to manage a mapping between sequences of tokens,
+ *     and their corresponding KV cache tensors" stored "in a non-contiguous,
+ *     paged layout, where the size of each page is equivalent to one token"
+ *     (P:180-181 [§3]); the tree "is stored on the CPU" (P:187 [§3]).
+ *     Pure host code; callable without a GPU.
+ *
+ *  2. device kernels over that pool (rx_store_kv, rx_extend, rx_decode):
+ *     causal attention of new tokens over "cached prefix + new KV" (extend,
+ *     prefill reuse, P:171, P:359 [§3, §6]) and of one token per request
+ *     (decode, P:495 [App. A.1]).  sm_100a only.  Asynchronous on the given
+ *     stream; the caller owns every device buffer and the stream; the library
+ *     never allocates device memory.
+ *
+ * Conventions
+ *  - Every call returns rx_status (0 = RX_OK, negative = error); no C++
+ *    exception crosses the ABI.  A failed call has no side effect unless
+ *    stated otherwise.
+ *  - Device pointers are marked d_, host pointers h_ (or unmarked for the
+ *    host-only tree calls).  bf16 buffers are passed as void*.
+ *  - Slot 0 of the pool is reserved as the padding sink (never allocated), so
+ *    allocatable slots are 1 .. num_slots-1.
+ *  - rx_cache is single-writer, not thread-safe.
+ *  - A launch failure is reported as RX_E_CUDA (cudaPeekAtLastError);
+ *    asynchronous device faults surface at the caller's next synchronisation.
+ */
+#ifndef RX_H_
+#define RX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RX_OK = 0,
+  RX_E_INVALID = -1,      /* bad argument (null pointer, negative size, out-of-range slot, ...) */
+  RX_E_NOMEM = -2,        /* rx_alloc: fewer free slots than requested (no side effect) */
+  RX_E_UNDERFLOW = -3,    /* rx_dec_ref would drive a reference count below 0 */
+  RX_E_STALE = -4,        /* node handle no longer names a live node */
+  RX_E_UNSUPPORTED = -5,  /* attention shape outside what the kernels implement */
+  RX_E_CUDA = -6,         /* a CUDA launch / driver call failed */
+  RX_E_WORKSPACE = -7,    /* workspace too small: query rx_*_workspace_bytes */
+  RX_E_CAPACITY = -8      /* a host output buffer is too small */
+} rx_status;
+
+/* Human-readable name of a status code (static string). */
+const char* rx_status_str(int status);
+
+/* Library build identification (static string): arch, build flags. */
+const char* rx_version(void);
+
+/* ======================================================================= */
+/*  1. Radix tree + token-slot pool (host)                                  */
+/* ======================================================================= */
+
+typedef struct rx_cache rx_cache;
+
+/* A node handle is the node's creation id (root = 0).  Ids are never reused,
+ * and a split keeps the id on the LOWER half (R4), so a handle stays valid
+ * until its node is evicted; a pinned node (ref > 0) is never evicted. */
+typedef int64_t rx_node;
+
+/* Create a tree + pool of num_slots token slots (num_slots >= 1; slot 0 is
+ * reserved).  One object owns both because "cached tokens and the currently
+ * running requests share the same memory pool" (P:184 [§3]).
+ * *out receives the new object; RX_E_INVALID if num_slots < 1 or out null. */
+rx_status rx_cache_create(int64_t num_slots, rx_cache** out);
+void rx_cache_destroy(rx_cache* c);
+
+/* Alg. 1 T.match_prefix (P:527 [App. A.2]).
+ * Longest prefix of tokens[0..n) present in the tree.  If the match ends in
+ * the middle of an edge the edge is split there (R3, R4).  The LRU clock ticks
+ * once and every node on the matched path is stamped (R1).
+ *   *node        deepest matched node (0 = root when nothing matches)
+ *   *matched_len number of matched tokens
+ *   slots_out    host int32[>= n]; receives the slots of the matched prefix
+ *                in position order (may be null).
+ * Never fails on content; empty tree or n == 0 -> (root, 0). */
+rx_status rx_match_prefix(rx_cache* c, const int32_t* tokens, int64_t n,
+                          rx_node* node, int64_t* matched_len, int32_t* slots_out);
+
+/* Alg. 1 T.insert (P:564 [App. A.2]).
+ * Cache tokens[0..n) with their slots[0..n).  Ownership of ALL passed slots
+ * moves to the cache: positions already cached keep the tree's slots, and a
+ * passed slot that differs there is freed, in position order (R10).
+ * The clock ticks once; the walked path and the new leaf are stamped (R1, R9).
+ *   *new_cached  tokens added to the tree (n minus the already-cached prefix)
+ *   *dup_freed   passed slots returned to the free pool (may be null) */
+rx_status rx_insert(rx_cache* c, const int32_t* tokens, const int32_t* slots, int64_t n,
+                    int64_t* new_cached, int64_t* dup_freed);
+
+/* Alg. 1 T.increase_ref_counter / decrease_ref_counter;
+ * SPEC S:131-139.  +/-1 on every node from `node` up to (excluding) the root.
+ * *d_evictable receives the change of rx_evictable_size (<= 0 for inc,
+ * >= 0 for dec).  RX_E_UNDERFLOW (no side effect) if a count would go below
+ * 0; RX_E_STALE for an evicted node. */
+rx_status rx_inc_ref(rx_cache* c, rx_node node, int64_t* d_evictable);
+rx_status rx_dec_ref(rx_cache* c, rx_node node, int64_t* d_evictable);
+
+/* Eviction callback: one call per evicted leaf, in eviction order, with that
+ * leaf's slots in position order (already returned to the free pool). */
+typedef void (*rx_evict_cb)(void* user, const int32_t* slots, int64_t n);
+
+/* "evicts the least recently used leaf first" (P:182 [§3]); Alg. 1 T.evict
+ * (P:554).  Removes whole leaves with ref 0 in
+ * (last_access, id) order (R2, R5); a parent left childless with ref 0
+ * becomes a candidate.  Stops when >= needed tokens were evicted or no
+ * candidate remains (falling short is NOT an error: compare *evicted).
+ * cb may be null. */
+rx_status rx_evict(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb, void* user);
+
+/* Token-slot pool.  rx_alloc returns the n smallest free slots in ascending
+ * order into out[0..n) (R8), or RX_E_NOMEM with no side effect.
+ * rx_free returns slots to the pool (RX_E_INVALID on a slot out of range or
+ * already free; then nothing is freed). */
+rx_status rx_alloc(rx_cache* c, int64_t n, int32_t* out);
+rx_status rx_free(rx_cache* c, const int32_t* slots, int64_t n);
+
+/* Alg. 1 lines 551-556 with reading R6: try rx_alloc(n); on
+ * RX_E_NOMEM evict the shortfall (n - available) and retry once.
+ * *evicted receives the tokens evicted (0 if none; may be null); cb as in
+ * rx_evict.  Returns RX_E_NOMEM if the retry still fails (the eviction is
+ * NOT undone). */
+rx_status rx_alloc_evict(rx_cache* c, int64_t n, int32_t* out, int64_t* evicted,
+                         rx_evict_cb cb, void* user);
+
+/* Pure queries (Alg. 1 "T.evictable_size() + P.available_size()", P:534;
+ * SPEC S:149-156).  evictable = tokens on non-root nodes with ref 0 (pins
+ * propagate to the root, so these are exactly the peelable nodes). */
+int64_t rx_evictable_size(const rx_cache* c);
+int64_t rx_total_cached(const rx_cache* c);
+int64_t rx_available(const rx_cache* c);
+int64_t rx_num_slots(const rx_cache* c);
+int64_t rx_clock(const rx_cache* c);
+
+/* Deterministic pre-order JSON dump: {"id","tokens","slots","ref",
+ * "last_access","children":[...]} with children ordered by first token.
+ * Writes at most cap bytes (NUL-terminated) into buf and returns the full
+ * length (excluding NUL); call with cap = 0 to size the buffer. */
+int64_t rx_dump_json(const rx_cache* c, char* buf, int64_t cap);
+
+/* ======================================================================= */
+/*  2. Attention over the token-slot KV pool (device, sm_100a)              */
+/* ======================================================================= */
+
+/* Shape of one attention call on one GPU (one TP shard, P:235 [§3]).
+ *   h_q       query heads in q / o           (this shard)
+ *   h_kv      KV heads in k_new / v_new / the pool slice (this shard)
+ *   head_dim  64 or 128
+ *   sm_scale  softmax scale, normally 1/sqrt(head_dim) (R12)
+ * GQA: q head h reads kv head h / (h_q / h_kv) (R14).  Supported: head_dim in
+ * {64, 128}, h_q % h_kv == 0, group size h_q/h_kv in {1, 2, 4, 8};
+ * otherwise RX_E_UNSUPPORTED.
+ *
+ * Layouts (all row-major, bf16):
+ *   pool      d_k_pool, d_v_pool : [num_slots, h_kv, head_dim]; a slot is one
+ *             contiguous row of all local heads (one token per page)
+ *   q, o      [tokens, h_q, head_dim]      k_new, v_new  [tokens, h_kv, head_dim]
+ *   req_to_token (rtt): int32 [rows, rtt_stride]; rtt[row][p] = slot of
+ *             position p of the request in that row (D10 in SURVEY §2).
+ *   d_rows    int32 [batch] or null: batch entry b uses rtt row d_rows[b]
+ *             (null: row b), so a persistent table is never re-uploaded.
+ */
+typedef struct {
+  int32_t h_q;
+  int32_t h_kv;
+  int32_t head_dim;
+  float sm_scale;
+} rx_attn_cfg;
+
+/* KV store: k_pool[slots[i]] = k[i]; v_pool[slots[i]] = v[i] for i < n
+ * (bit-exact copy).  If d_rtt_index is non-null, also rtt_flat[d_rtt_index[i]]
+ * = slots[i] (d_rtt must then be non-null): the decode step's "append one
+ * column to req_to_token" in the same launch.  Slots must be distinct and in
+ * [1, num_slots).  Asynchronous on stream. */
+rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
+                      const void* d_k, const void* d_v, void* d_k_pool, void* d_v_pool,
+                      int64_t num_slots, int32_t* d_rtt, const int64_t* d_rtt_index,
+                      void* stream);
+
+/* Extend (prefill with prefix reuse) for a ragged batch.
+ * Request b has prefix_len[b] cached tokens (slots rtt[row_b][0..prefix_len))
+ * and extend_len[b] >= 0 new tokens at positions prefix_len .. prefix_len +
+ * extend_len - 1, whose slots are rtt[row_b][prefix_len + j].  The call
+ *   (1) stores k_new / v_new of every new token into its slot, and
+ *   (2) for new token j at absolute position p = prefix_len + j and q head h,
+ *       o = softmax_{i <= p}(scale * q . K[i]) V[i]   over the kv head of h
+ *       (R13: causal over absolute positions; fp32 accumulation, R15).
+ * Hazard-free in one call because new slots are never prefix slots.
+ *   d_prefix_lens, d_extend_lens : int32 [batch]        (device)
+ *   d_qo_indptr                  : int32 [batch + 1]    (device) exclusive
+ *       prefix sum of extend_lens: request b's rows in q/k_new/v_new/o are
+ *       [qo_indptr[b], qo_indptr[b+1])
+ *   total_new        = qo_indptr[batch] (host copy, sizes the TMA views)
+ *   max_extend_len   = max extend_len (host copy, sizes the grid)
+ *   max_prefix_len   = max prefix_len (host copy)
+ * Workspace: d_ws of ws_bytes >= rx_extend_workspace_bytes(...). */
+rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch,
+                    const int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
+                    const int32_t* d_prefix_lens, const int32_t* d_extend_lens,
+                    const int32_t* d_qo_indptr, int64_t total_new,
+                    int32_t max_extend_len, int32_t max_prefix_len,
+                    const void* d_q, const void* d_k_new, const void* d_v_new,
+                    void* d_k_pool, void* d_v_pool, int64_t num_slots, void* d_o,
+                    void* d_ws, size_t ws_bytes, void* stream);
+
+size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len);
+
+/* Decode: one query per request at position seq_len[b] - 1 (P:495 [App.
+ * A.1]), over slots rtt[row_b][0 .. seq_len[b]).  The newest token's KV must
+ * already be stored (rx_store_kv) and seq_len counts it; seq_len >= 1
+ * (entries < 1 produce undefined rows: validate on the host).
+ *   d_seq_lens  int32 [batch] (device);  max_seq_len = its max (host copy;
+ *   plans the split-KV partition, so it must be >= every seq_len).
+ * Split-KV partials are merged by log-sum-exp in the same call (A8).
+ * Workspace: d_ws of ws_bytes >= rx_decode_workspace_bytes(...). */
+rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch,
+                    const int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
+                    const int32_t* d_seq_lens, int32_t max_seq_len,
+                    const void* d_q, const void* d_k_pool, const void* d_v_pool,
+                    int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream);
+
+size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len);
+
+/* Number of kernel launches the last successful rx_extend / rx_decode /
+ * rx_store_kv call on this thread issued (for launch accounting). */
+int32_t rx_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RX_H_ */

@@ -61,7 +61,7 @@ class Seq:
 
 
 class OracleEngine:
-    def __init__(self, wl, sample_extend=None, sample_decode=None, q_scale=1.0):
+    def __init__(self, wl, sample_extend=None, sample_decode=None, q_scale=1.0, materialize=False):
         """sample_extend(call_idx, B, prefix_lens, extend_lens) -> list of (req_idx, j) rows to evaluate, or None (= none);
         sample_decode(call_idx, step, B) -> list of req_idx to evaluate."""
         self.wl = wl
@@ -76,9 +76,25 @@ class OracleEngine:
         self.decode_calls = 0
         self.outputs = {}           # ("extend", call, req_idx, j) / ("decode", call, req_idx) -> float64 [H_q, hd]
         self.stats = {"prompt_tokens": 0, "cached_prompt_tokens": 0}
+        # materialize=True: the pool holds expanded K/V values (written at store time);
+        # False: it holds the prefix hash per slot and expands on read (full-size sampled runs)
+        self.pool = attention.OraclePool(wl.num_slots, wl.shape.h_kv, wl.shape.head_dim) if materialize else None
 
     # ------------------------------------------------------------ pool / values
+    def _store(self, slots, hashes):
+        for s_, h in zip(slots, hashes):
+            self.slot_hash[int(s_)] = int(h)
+        if self.pool is not None and len(slots):
+            hs = np.asarray(hashes, dtype=np.uint64)
+            sh = self.shape
+            k = gen_values(hs, range(sh.h_kv), KIND_K, sh.head_dim).float().numpy()
+            v = gen_values(hs, range(sh.h_kv), KIND_V, sh.head_dim).float().numpy()
+            self.pool.store(np.asarray(slots, dtype=np.int64), k, v)
+
     def _kv(self, slots, g, kind):
+        if self.pool is not None:
+            arr = self.pool.k if kind == KIND_K else self.pool.v
+            return arr[np.asarray(slots, dtype=np.int64), g].astype(np.float64)
         hs = np.array([self.slot_hash[int(s)] for s in slots], dtype=np.uint64)
         return gen_values(hs, [g], kind, self.shape.head_dim)[:, 0].float().numpy().astype(np.float64)
 
@@ -147,9 +163,8 @@ class OracleEngine:
         # 4. extend: store new KV (slot -> prefix hash), then attend
         call = self.extend_calls
         self.extend_calls += 1
-        for s in seqs:
-            for p in range(s.prefix_len, s.n_prompt):
-                self.slot_hash[s.slots[p]] = s.hashes[p]
+        self._store([s.slots[p] for s in seqs for p in range(s.prefix_len, s.n_prompt)],
+                    [s.hashes[p] for s in seqs for p in range(s.prefix_len, s.n_prompt)])
         rows = self.sample_extend(call, seqs) if self.sample_extend else []
         for (bi, j) in rows:
             s = seqs[bi]
@@ -166,7 +181,7 @@ class OracleEngine:
             new = self._alloc(len(running))
             for s, slot in zip(running, new):
                 s.slots.append(slot)
-                self.slot_hash[slot] = s.hashes[-1]
+            self._store(new, [s.hashes[-1] for s in running])
             call = self.decode_calls
             self.decode_calls += 1
             idx = self.sample_decode(call, step, running) if self.sample_decode else []

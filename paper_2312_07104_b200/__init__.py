@@ -1,0 +1,13 @@
+"""B200-native RadixAttention hot path (arXiv 2312.07104).
+
+librx.so (C ABI, include/rx.h): host radix tree over a token-slot KV pool +
+sm_100a kernels for KV store, extend (tcgen05/TMEM) and decode (split-KV,
+GQA-grouped).  This package is the thin Python binding plus the request-flow
+harness that drives it.  It never imports ``oracle/``.
+"""
+from .api import (RadixCache, attn_cfg, rx_store_kv, rx_extend, rx_decode, rx_extend_workspace_bytes,
+                  rx_decode_workspace_bytes, rx_last_launch_count)
+from ._lib import RxError, LIB_PATH
+
+__all__ = ["RadixCache", "attn_cfg", "rx_store_kv", "rx_extend", "rx_decode", "rx_extend_workspace_bytes",
+           "rx_decode_workspace_bytes", "rx_last_launch_count", "RxError", "LIB_PATH"]

@@ -1,0 +1,72 @@
+"""ctypes declarations for librx.so (include/rx.h).  Argument marshalling only.
+
+Loading fails loudly (ImportError) if the in-tree library is missing: there is
+no fallback path of any kind.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librx.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2312_07104_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+
+lib = C.CDLL(LIB_PATH)
+
+i32, i64, f32, vp, sz = C.c_int32, C.c_int64, C.c_float, C.c_void_p, C.c_size_t
+P32 = C.POINTER(C.c_int32)
+P64 = C.POINTER(C.c_int64)
+
+
+class AttnCfg(C.Structure):
+    _fields_ = [("h_q", i32), ("h_kv", i32), ("head_dim", i32), ("sm_scale", f32)]
+
+
+EVICT_CB = C.CFUNCTYPE(None, vp, P32, i64)
+
+# symbol -> (restype, argtypes); the set of names is exactly include/rx.h's declarations
+SIGNATURES = {
+    "rx_status_str": (C.c_char_p, [C.c_int]),
+    "rx_version": (C.c_char_p, []),
+    "rx_cache_create": (C.c_int, [i64, C.POINTER(vp)]),
+    "rx_cache_destroy": (None, [vp]),
+    "rx_match_prefix": (C.c_int, [vp, P32, i64, P64, P64, P32]),
+    "rx_insert": (C.c_int, [vp, P32, P32, i64, P64, P64]),
+    "rx_inc_ref": (C.c_int, [vp, i64, P64]),
+    "rx_dec_ref": (C.c_int, [vp, i64, P64]),
+    "rx_evict": (C.c_int, [vp, i64, P64, EVICT_CB, vp]),
+    "rx_alloc": (C.c_int, [vp, i64, P32]),
+    "rx_free": (C.c_int, [vp, P32, i64]),
+    "rx_alloc_evict": (C.c_int, [vp, i64, P32, P64, EVICT_CB, vp]),
+    "rx_evictable_size": (i64, [vp]),
+    "rx_total_cached": (i64, [vp]),
+    "rx_available": (i64, [vp]),
+    "rx_num_slots": (i64, [vp]),
+    "rx_clock": (i64, [vp]),
+    "rx_dump_json": (i64, [vp, C.c_char_p, i64]),
+    "rx_store_kv": (C.c_int, [C.POINTER(AttnCfg), i64, vp, vp, vp, vp, vp, i64, vp, vp, vp]),
+    "rx_extend": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, vp, i64, i32, i32,
+                            vp, vp, vp, vp, vp, i64, vp, vp, sz, vp]),
+    "rx_extend_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
+    "rx_decode": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, i64, vp, vp, sz, vp]),
+    "rx_decode_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
+    "rx_last_launch_count": (i32, []),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+STATUS = {0: "RX_OK", -1: "RX_E_INVALID", -2: "RX_E_NOMEM", -3: "RX_E_UNDERFLOW", -4: "RX_E_STALE",
+          -5: "RX_E_UNSUPPORTED", -6: "RX_E_CUDA", -7: "RX_E_WORKSPACE", -8: "RX_E_CAPACITY"}
+
+
+class RxError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {STATUS.get(status, status)}")
+        self.status = status

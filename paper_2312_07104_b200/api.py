@@ -1,0 +1,209 @@
+"""Python binding of librx.so: same names as include/rx.h, argument marshalling only.
+
+* ``RadixCache`` wraps ``rx_cache`` (host radix tree + token-slot pool).
+* ``rx_store_kv`` / ``rx_extend`` / ``rx_decode`` take torch CUDA tensors and
+  launch on the current torch stream.  Every step runs in librx's kernels;
+  torch supplies device memory and the stream only.  Wrong device / dtype /
+  layout raises — there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+
+from ._lib import lib, AttnCfg, EVICT_CB, RxError, P32, P64
+
+_I32 = np.int32
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=_I32)
+
+
+def _p32(a: np.ndarray):
+    return a.ctypes.data_as(P32)
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise RxError(st, what)
+
+
+class RadixCache:
+    """rx_cache: the radix tree and the token-slot pool it shares with running requests."""
+
+    def __init__(self, num_slots: int):
+        h = C.c_void_p()
+        _check(lib.rx_cache_create(num_slots, C.byref(h)), "rx_cache_create")
+        self._h = h
+        self.num_slots = num_slots
+        self._runs = []
+        self._cb = EVICT_CB(self._on_evict)
+
+    def close(self):
+        if self._h:
+            lib.rx_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _on_evict(self, user, slots, n):
+        self._runs.append(np.ctypeslib.as_array(slots, shape=(n,)).copy() if n else np.zeros(0, _I32))
+
+    # -------------------------------------------------------------- tree
+    def rx_match_prefix(self, tokens):
+        """-> (node handle, matched_len, slots int32[matched_len])"""
+        t = _i32(tokens)
+        out = np.empty(max(len(t), 1), dtype=_I32)
+        node, m = C.c_int64(), C.c_int64()
+        _check(lib.rx_match_prefix(self._h, _p32(t), len(t), C.byref(node), C.byref(m), _p32(out)),
+               "rx_match_prefix")
+        return node.value, m.value, out[:m.value]
+
+    def rx_insert(self, tokens, slots):
+        """-> (new_cached, dup_freed)"""
+        t, s = _i32(tokens), _i32(slots)
+        if len(t) != len(s):
+            raise ValueError("tokens/slots length mismatch")
+        nc, nd = C.c_int64(), C.c_int64()
+        _check(lib.rx_insert(self._h, _p32(t), _p32(s), len(t), C.byref(nc), C.byref(nd)), "rx_insert")
+        return nc.value, nd.value
+
+    def rx_inc_ref(self, node: int) -> int:
+        d = C.c_int64()
+        _check(lib.rx_inc_ref(self._h, node, C.byref(d)), "rx_inc_ref")
+        return d.value
+
+    def rx_dec_ref(self, node: int) -> int:
+        d = C.c_int64()
+        _check(lib.rx_dec_ref(self._h, node, C.byref(d)), "rx_dec_ref")
+        return d.value
+
+    def rx_evict(self, needed: int):
+        """-> (evicted tokens, [slot runs in eviction order])"""
+        self._runs = []
+        ev = C.c_int64()
+        _check(lib.rx_evict(self._h, needed, C.byref(ev), self._cb, None), "rx_evict")
+        return ev.value, self._runs
+
+    def rx_alloc(self, n: int):
+        """n smallest free slots (ascending) or None on RX_E_NOMEM."""
+        out = np.empty(max(n, 1), dtype=_I32)
+        st = lib.rx_alloc(self._h, n, _p32(out))
+        if st == -2:
+            return None
+        _check(st, "rx_alloc")
+        return out[:n]
+
+    def rx_alloc_evict(self, n: int):
+        """Alg. 1 alloc -> evict shortfall -> retry.  -> (slots or None, evicted, runs)"""
+        self._runs = []
+        out = np.empty(max(n, 1), dtype=_I32)
+        ev = C.c_int64()
+        st = lib.rx_alloc_evict(self._h, n, _p32(out), C.byref(ev), self._cb, None)
+        if st == -2:
+            return None, ev.value, self._runs
+        _check(st, "rx_alloc_evict")
+        return out[:n], ev.value, self._runs
+
+    def rx_free(self, slots):
+        s = _i32(slots)
+        _check(lib.rx_free(self._h, _p32(s), len(s)), "rx_free")
+
+    def rx_evictable_size(self) -> int:
+        return lib.rx_evictable_size(self._h)
+
+    def rx_total_cached(self) -> int:
+        return lib.rx_total_cached(self._h)
+
+    def rx_available(self) -> int:
+        return lib.rx_available(self._h)
+
+    def rx_clock(self) -> int:
+        return lib.rx_clock(self._h)
+
+    def rx_dump_json(self) -> dict:
+        n = lib.rx_dump_json(self._h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib.rx_dump_json(self._h, buf, n + 1)
+        return json.loads(buf.value.decode())
+
+
+# ------------------------------------------------------------------ device calls
+def attn_cfg(h_q: int, h_kv: int, head_dim: int, sm_scale: float) -> AttnCfg:
+    return AttnCfg(h_q, h_kv, head_dim, sm_scale)
+
+
+def _dev(t, dtype=None, name="tensor"):
+    import torch
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def rx_store_kv(cfg: AttnCfg, slots, k, v, k_pool, v_pool, rtt=None, rtt_index=None, stream=None):
+    import torch
+    n = slots.shape[0]
+    st = lib.rx_store_kv(C.byref(cfg), n, _dev(slots, torch.int32, "slots"), _dev(k, torch.bfloat16, "k"),
+                         _dev(v, torch.bfloat16, "v"), _dev(k_pool, torch.bfloat16, "k_pool"),
+                         _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0],
+                         _dev(rtt, torch.int32, "rtt"), _dev(rtt_index, torch.int64, "rtt_index"), _stream(stream))
+    _check(st, "rx_store_kv")
+
+
+def rx_extend_workspace_bytes(cfg: AttnCfg, batch: int, max_extend_len: int) -> int:
+    return lib.rx_extend_workspace_bytes(C.byref(cfg), batch, max_extend_len)
+
+
+def rx_decode_workspace_bytes(cfg: AttnCfg, batch: int, max_seq_len: int) -> int:
+    return lib.rx_decode_workspace_bytes(C.byref(cfg), batch, max_seq_len)
+
+
+def rx_extend(cfg: AttnCfg, rtt, rows, prefix_lens, extend_lens, qo_indptr, total_new: int, max_extend_len: int,
+              max_prefix_len: int, q, k_new, v_new, k_pool, v_pool, o, ws=None, stream=None):
+    import torch
+    batch = prefix_lens.shape[0]
+    ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    st = lib.rx_extend(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
+                       _dev(rows, torch.int32, "rows"), _dev(prefix_lens, torch.int32, "prefix_lens"),
+                       _dev(extend_lens, torch.int32, "extend_lens"), _dev(qo_indptr, torch.int32, "qo_indptr"),
+                       total_new, max_extend_len, max_prefix_len, _dev(q, torch.bfloat16, "q"),
+                       _dev(k_new, torch.bfloat16, "k_new"), _dev(v_new, torch.bfloat16, "v_new"),
+                       _dev(k_pool, torch.bfloat16, "k_pool"), _dev(v_pool, torch.bfloat16, "v_pool"),
+                       k_pool.shape[0], _dev(o, torch.bfloat16, "o"), _dev(ws, None, "ws"), ws_bytes,
+                       _stream(stream))
+    _check(st, "rx_extend")
+
+
+def rx_decode(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int, q, k_pool, v_pool, o, ws=None, stream=None):
+    import torch
+    batch = seq_lens.shape[0]
+    ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    st = lib.rx_decode(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
+                       _dev(rows, torch.int32, "rows"), _dev(seq_lens, torch.int32, "seq_lens"), max_seq_len,
+                       _dev(q, torch.bfloat16, "q"), _dev(k_pool, torch.bfloat16, "k_pool"),
+                       _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0], _dev(o, torch.bfloat16, "o"),
+                       _dev(ws, None, "ws"), ws_bytes, _stream(stream))
+    _check(st, "rx_decode")
+
+
+def rx_last_launch_count() -> int:
+    return lib.rx_last_launch_count()

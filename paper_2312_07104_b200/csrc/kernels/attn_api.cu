@@ -1,0 +1,153 @@
+// C-ABI entry points for the device half of include/rx.h: argument checks,
+// planning, and the launches of store.cu / extend.cu / decode.cu.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../../include/rx.h"
+
+#include "params.cuh"
+
+namespace {
+thread_local int32_t g_last_launches = 0;
+
+rx_status check_cfg(const rx_attn_cfg* c) {
+  if (!c || c->h_q <= 0 || c->h_kv <= 0) return RX_E_INVALID;
+  if (c->h_q % c->h_kv) return RX_E_UNSUPPORTED;
+  const int G = c->h_q / c->h_kv;
+  if (!(c->head_dim == 64 || c->head_dim == 128)) return RX_E_UNSUPPORTED;
+  if (!(G == 1 || G == 2 || G == 4 || G == 8)) return RX_E_UNSUPPORTED;
+  return RX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* rx_status_str(int s) {
+  switch (s) {
+    case RX_OK: return "RX_OK";
+    case RX_E_INVALID: return "RX_E_INVALID";
+    case RX_E_NOMEM: return "RX_E_NOMEM";
+    case RX_E_UNDERFLOW: return "RX_E_UNDERFLOW";
+    case RX_E_STALE: return "RX_E_STALE";
+    case RX_E_UNSUPPORTED: return "RX_E_UNSUPPORTED";
+    case RX_E_CUDA: return "RX_E_CUDA";
+    case RX_E_WORKSPACE: return "RX_E_WORKSPACE";
+    case RX_E_CAPACITY: return "RX_E_CAPACITY";
+    default: return "RX_E_UNKNOWN";
+  }
+}
+
+const char* rx_version(void) { return "rx 0.1 sm_100a (tcgen05 extend, mma.sync decode)"; }
+
+int32_t rx_last_launch_count(void) { return g_last_launches; }
+
+rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots, const void* d_k, const void* d_v,
+                      void* d_k_pool, void* d_v_pool, int64_t num_slots, int32_t* d_rtt,
+                      const int64_t* d_rtt_index, void* stream) {
+  rx_status s = check_cfg(cfg);
+  if (s != RX_OK) return s;
+  if (n < 0 || num_slots < 1) return RX_E_INVALID;
+  if (n > 0 && (!d_slots || !d_k || !d_v || !d_k_pool || !d_v_pool)) return RX_E_INVALID;
+  if (d_rtt_index && !d_rtt) return RX_E_INVALID;
+  g_last_launches = 0;
+  if (n == 0) return RX_OK;
+  cudaError_t e = rx::launch_store_kv(n, cfg->h_kv * cfg->head_dim * 2, d_slots, d_k, d_v, d_k_pool, d_v_pool,
+                                      d_rtt, d_rtt_index, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return RX_E_CUDA;
+  g_last_launches = 1;
+  return RX_OK;
+}
+
+size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len) {
+  if (check_cfg(cfg) != RX_OK || batch <= 0 || max_seq_len <= 0) return 0;
+  return rx::decode_ws_bytes(cfg->h_q, cfg->head_dim, batch, max_seq_len, cfg->h_kv);
+}
+
+rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
+                    const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
+                    const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
+                    size_t ws_bytes, void* stream) {
+  rx_status s = check_cfg(cfg);
+  if (s != RX_OK) return s;
+  if (batch < 0 || max_seq_len < 0 || num_slots < 1) return RX_E_INVALID;
+  g_last_launches = 0;
+  if (batch == 0) return RX_OK;
+  if (max_seq_len < 1 || !d_rtt || !d_seq_lens || !d_q || !d_k_pool || !d_v_pool || !d_o) return RX_E_INVALID;
+  if (rtt_stride < max_seq_len) return RX_E_INVALID;
+  const size_t need = rx::decode_ws_bytes(cfg->h_q, cfg->head_dim, batch, max_seq_len, cfg->h_kv);
+  if (need > 0 && (!d_ws || ws_bytes < need)) return RX_E_WORKSPACE;
+  rx::DecodePlan pl = rx::plan_decode(batch, cfg->h_kv, max_seq_len);
+  rx::DecodeParams p{};
+  p.q = static_cast<const __nv_bfloat16*>(d_q);
+  p.kpool = static_cast<const __nv_bfloat16*>(d_k_pool);
+  p.vpool = static_cast<const __nv_bfloat16*>(d_v_pool);
+  p.o = static_cast<__nv_bfloat16*>(d_o);
+  p.rtt = d_rtt;
+  p.rtt_stride = rtt_stride;
+  p.rows = d_rows;
+  p.seq_lens = d_seq_lens;
+  const size_t n = size_t(batch) * cfg->h_q * pl.max_splits;
+  p.ws_o = static_cast<float*>(d_ws);
+  p.ws_lse = need ? reinterpret_cast<float*>(static_cast<char*>(d_ws) + n * cfg->head_dim * sizeof(float)) : nullptr;
+  p.h_q = cfg->h_q;
+  p.h_kv = cfg->h_kv;
+  p.chunk = pl.chunk;
+  p.max_splits = pl.max_splits;
+  p.scale_log2 = cfg->sm_scale * 1.4426950408889634f;
+  int launches = 0;
+  cudaError_t e = rx::launch_decode(cfg->head_dim, cfg->h_q / cfg->h_kv, p, batch,
+                                    static_cast<cudaStream_t>(stream), &launches);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  g_last_launches = launches;
+  return RX_OK;
+}
+
+size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len) {
+  (void)cfg;
+  (void)batch;
+  (void)max_extend_len;
+  return 0;
+}
+
+rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
+                    const int32_t* d_rows, const int32_t* d_prefix_lens, const int32_t* d_extend_lens,
+                    const int32_t* d_qo_indptr, int64_t total_new, int32_t max_extend_len, int32_t max_prefix_len,
+                    const void* d_q, const void* d_k_new, const void* d_v_new, void* d_k_pool, void* d_v_pool,
+                    int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
+  (void)d_ws;
+  (void)ws_bytes;
+  rx_status s = check_cfg(cfg);
+  if (s != RX_OK) return s;
+  if (batch < 0 || total_new < 0 || max_extend_len < 0 || max_prefix_len < 0 || num_slots < 1)
+    return RX_E_INVALID;
+  g_last_launches = 0;
+  if (batch == 0 || total_new == 0 || max_extend_len == 0) return RX_OK;
+  if (!d_rtt || !d_prefix_lens || !d_extend_lens || !d_qo_indptr || !d_q || !d_k_new || !d_v_new || !d_k_pool ||
+      !d_v_pool || !d_o)
+    return RX_E_INVALID;
+  if (rtt_stride < int64_t(max_prefix_len) + max_extend_len) return RX_E_INVALID;
+  rx::ExtendParams p{};
+  p.rtt = d_rtt;
+  p.rtt_stride = rtt_stride;
+  p.rows = d_rows;
+  p.prefix_lens = d_prefix_lens;
+  p.extend_lens = d_extend_lens;
+  p.qo_indptr = d_qo_indptr;
+  p.k_new = static_cast<const __nv_bfloat16*>(d_k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(d_v_new);
+  p.kpool = static_cast<__nv_bfloat16*>(d_k_pool);
+  p.vpool = static_cast<__nv_bfloat16*>(d_v_pool);
+  p.o = static_cast<__nv_bfloat16*>(d_o);
+  p.h_q = cfg->h_q;
+  p.h_kv = cfg->h_kv;
+  p.num_slots = num_slots;
+  p.scale_log2 = cfg->sm_scale * 1.4426950408889634f;
+  cudaError_t e = rx::launch_extend(cfg->head_dim, cfg->h_q / cfg->h_kv, p, d_q, total_new, batch, max_extend_len,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return RX_E_CUDA;
+  g_last_launches = 1;
+  return RX_OK;
+}
+
+}  // extern "C"

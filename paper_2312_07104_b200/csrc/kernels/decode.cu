@@ -1,0 +1,283 @@
+// Decode attention over the token-slot KV pool (rx_decode, include/rx.h).
+//
+// Computes, for each request b and q head h (kv head g = h / G, R14):
+//     o = softmax_{i < seq_len}(scale * q . K[rtt[b][i]]) V[rtt[b][i]]
+// i.e. one query per request at position seq_len-1 (App. A.1),
+// reading the cached prefix through the slot table (one token per page,
+// PAPER.md:181 §3).
+//
+// B200 design (HBM-bound; 2*G FLOP per K/V byte pair):
+//  * one CTA per (split, kv head, request); 4 warps each stream their own
+//    16-token blocks of the split through a private STAGES-deep cp.async
+//    pipeline (16-byte gathers of pool rows by slot, XOR-swizzled smem);
+//  * the G query heads of one kv head share every K/V byte (GQA grouping):
+//    S^T[16 tok x 8 heads] = K[16 x hd] . Q^T on mma.sync m16n8k16 (heads
+//    padded to 8 — G <= 8 so at most 8x waste, still far below the HMMA
+//    rate), online softmax in registers, P^T re-fragmented with movmatrix,
+//    O^T[hd x 8] += V^T . P^T;
+//  * warps merge through shared memory; splits merge by log-sum-exp in a
+//    second small kernel (A8), or the CTA writes bf16 output directly when
+//    the request has a single split.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "params.cuh"
+#include "ptx.cuh"
+
+namespace rx {
+
+constexpr int kDecWarps = 4;
+constexpr int kBlk = 16;
+
+template <int HD>
+struct DecCfg {
+  static constexpr int RB = HD * 2;                   // bytes per row
+  static constexpr int BLK_BYTES = kBlk * RB;         // one K (or V) block
+  static constexpr int STAGES = HD == 128 ? 4 : 6;
+  static constexpr int WARP_BYTES = STAGES * 2 * BLK_BYTES;
+  static constexpr int SMEM = kDecWarps * WARP_BYTES;
+  static constexpr int CHUNKS = kBlk * HD / 8;        // 16-byte chunks per block
+  static_assert(SMEM >= kDecWarps * HD * 8 * 4, "merge scratch must fit");
+};
+
+template <int HD>
+__device__ __forceinline__ void dec_issue_block(uint32_t kdst, uint32_t vdst, const __nv_bfloat16* kpool,
+                                                const __nv_bfloat16* vpool, int slot, int h_kv, int g) {
+  constexpr int CPR = HD / 8;  // chunks per row
+  const int lane = lane_id();
+#pragma unroll
+  for (int c = 0; c < DecCfg<HD>::CHUNKS / 32; ++c) {
+    const int idx = c * 32 + lane;
+    const int r = idx / CPR, ch = idx % CPR;
+    const int sl = __shfl_sync(0xffffffffu, slot, r);
+    const bool ok = sl > 0;
+    const int64_t off = (int64_t(ok ? sl : 0) * h_kv + g) * HD + ch * 8;
+    const uint32_t so = r * DecCfg<HD>::RB + ((ch ^ (r & 7)) << 4);
+    cp_async_16(kdst + so, kpool + off, ok ? 16u : 0u);
+    cp_async_16(vdst + so, vpool + off, ok ? 16u : 0u);
+  }
+}
+
+template <int HD, int G>
+__global__ void __launch_bounds__(kDecWarps * 32) decode_kernel(const DecodeParams p) {
+  using C = DecCfg<HD>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int b = blockIdx.z, g = blockIdx.y, s = blockIdx.x;
+  const int L = p.seq_lens[b];
+  const int start = s * p.chunk;
+  if (start >= L) return;
+  const int end = min(L, start + p.chunk);
+  const int nsplit = (L + p.chunk - 1) / p.chunk;
+  const int row = p.rows ? p.rows[b] : b;
+  const int32_t* slots = p.rtt + int64_t(row) * p.rtt_stride;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  // Q^T fragments (B operand): b0 = Q[head gq][16kk + 2tq .. +1], b1 = Q[head gq][16kk + 8 + 2tq .. +1]
+  uint32_t qf[HD / 16][2];
+  {
+    const __nv_bfloat16* qrow = p.q + (int64_t(b) * p.h_q + g * G + gq) * HD;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      if (gq < G) {
+        qf[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tq);
+        qf[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tq);
+      } else {
+        qf[kk][0] = qf[kk][1] = 0u;
+      }
+    }
+  }
+
+  const uint32_t wbase = smem_u32(smem) + warp * C::WARP_BYTES;
+  auto kst = [&](int st) { return wbase + st * 2 * C::BLK_BYTES; };
+  auto vst = [&](int st) { return wbase + st * 2 * C::BLK_BYTES + C::BLK_BYTES; };
+
+  const int nblk = (end - start + kBlk - 1) / kBlk;
+  const int my = warp < nblk ? (nblk - warp + kDecWarps - 1) / kDecWarps : 0;
+  auto tok0 = [&](int i) { return start + (warp + i * kDecWarps) * kBlk; };
+  auto load_slot = [&](int i) -> int {
+    if (i >= my || lane >= kBlk) return 0;
+    const int t = tok0(i) + lane;
+    return t < end ? slots[t] : 0;
+  };
+
+#pragma unroll
+  for (int st = 0; st < C::STAGES - 1; ++st) {
+    const int sl = load_slot(st);
+    if (st < my) dec_issue_block<HD>(kst(st), vst(st), p.kpool, p.vpool, sl, p.h_kv, g);
+    cp_async_commit();
+  }
+  int slot_pref = load_slot(C::STAGES - 1);
+
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  float oacc[HD / 16][4];
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+
+  for (int i = 0; i < my; ++i) {
+    {
+      const int ii = i + C::STAGES - 1;
+      if (ii < my) dec_issue_block<HD>(kst(ii % C::STAGES), vst(ii % C::STAGES), p.kpool, p.vpool, slot_pref,
+                                       p.h_kv, g);
+      cp_async_commit();
+      slot_pref = load_slot(i + C::STAGES);
+    }
+    cp_async_wait<C::STAGES - 1>();
+    __syncwarp();
+    const int st = i % C::STAGES;
+    const uint32_t kb = kst(st), vb = vst(st);
+    const int nvalid = end - tok0(i);
+
+    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int ch = 2 * kk + (lane >> 4);
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(kb + r * C::RB + ((ch ^ (r & 7)) << 4), a0, a1, a2, a3);
+        mma_bf16_16816(sacc, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+      }
+    }
+    // scale into log2 domain; mask tokens past the end of the split
+    float s0 = gq < nvalid ? sacc[0] * p.scale_log2 : -INFINITY;
+    float s1 = gq < nvalid ? sacc[1] * p.scale_log2 : -INFINITY;
+    float s2 = gq + 8 < nvalid ? sacc[2] * p.scale_log2 : -INFINITY;
+    float s3 = gq + 8 < nvalid ? sacc[3] * p.scale_log2 : -INFINITY;
+    float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float c0 = fast_exp2(m0 - mn0), c1 = fast_exp2(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    const float p0 = fast_exp2(s0 - mn0), p1 = fast_exp2(s1 - mn1);
+    const float p2 = fast_exp2(s2 - mn0), p3 = fast_exp2(s3 - mn1);
+    l0 = l0 * c0 + p0 + p2;
+    l1 = l1 * c1 + p1 + p3;
+#pragma unroll
+    for (int mt = 0; mt < HD / 16; ++mt) {
+      oacc[mt][0] *= c0;
+      oacc[mt][1] *= c1;
+      oacc[mt][2] *= c0;
+      oacc[mt][3] *= c1;
+    }
+    const uint32_t bx = movmatrix_trans(pack_bf16(p0, p1));
+    const uint32_t by = movmatrix_trans(pack_bf16(p2, p3));
+    {
+      const int m = lane >> 3;
+      const int r = (lane & 7) + (m >> 1) * 8;
+#pragma unroll
+      for (int mt = 0; mt < HD / 16; ++mt) {
+        const int ch = 2 * mt + (m & 1);
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4_trans(vb + r * C::RB + ((ch ^ (r & 7)) << 4), a0, a1, a2, a3);
+        mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bx, by);
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  __syncthreads();  // all warps done with their pipelines: reuse smem for the merge
+
+  float* opart = reinterpret_cast<float*>(smem);                  // [warps][HD][8]
+  __shared__ float red_m[kDecWarps][8], red_l[kDecWarps][8];
+  if (gq == 0) {
+    red_m[warp][2 * tq] = m0;
+    red_m[warp][2 * tq + 1] = m1;
+    red_l[warp][2 * tq] = l0;
+    red_l[warp][2 * tq + 1] = l1;
+  }
+  float* ow = opart + warp * HD * 8;
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    const int d = 16 * mt + gq;
+    ow[d * 8 + 2 * tq] = oacc[mt][0];
+    ow[d * 8 + 2 * tq + 1] = oacc[mt][1];
+    ow[(d + 8) * 8 + 2 * tq] = oacc[mt][2];
+    ow[(d + 8) * 8 + 2 * tq + 1] = oacc[mt][3];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * HD; idx += kDecWarps * 32) {
+    const int h = idx / HD, d = idx % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, red_m[w][h]);
+    float acc = 0.f, Ls = 0.f;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) {
+      const float f = fast_exp2(red_m[w][h] - M);
+      Ls += f * red_l[w][h];
+      acc += f * opart[(w * HD + d) * 8 + h];
+    }
+    const int hq = g * G + h;
+    if (nsplit == 1) {
+      p.o[(int64_t(b) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / Ls);
+    } else {
+      const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits + s;
+      p.ws_o[base * HD + d] = acc / Ls;
+      if (d == 0) p.ws_lse[base] = M + __log2f(Ls);
+    }
+  }
+}
+
+// Log-sum-exp merge of split partials (A8): o = sum_s 2^(lse_s - LSE) o_s.
+template <int HD>
+__global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p) {
+  const int b = blockIdx.x, hq = blockIdx.y;
+  const int L = p.seq_lens[b];
+  const int nsplit = (L + p.chunk - 1) / p.chunk;
+  if (nsplit <= 1) return;
+  const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits;
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, p.ws_lse[base + s]);
+  float W = 0.f;
+  for (int s = 0; s < nsplit; ++s) W += fast_exp2(p.ws_lse[base + s] - M);
+  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < nsplit; ++s) acc += fast_exp2(p.ws_lse[base + s] - M) * p.ws_o[(base + s) * HD + d];
+    p.o[(int64_t(b) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / W);
+  }
+}
+
+template <int HD, int G>
+static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_t st, int* launches) {
+  using C = DecCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  dim3 grid(p.max_splits, p.h_kv, batch);
+  decode_kernel<HD, G><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);
+  *launches = 1;
+  if (p.max_splits > 1) {
+    decode_merge_kernel<HD><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
+    *launches = 2;
+  }
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st,
+                          int* launches) {
+#define RX_DEC_CASE(HD_, G_) \
+  if (head_dim == HD_ && G == G_) return launch_decode_t<HD_, G_>(p, batch, st, launches);
+  RX_DEC_CASE(64, 1) RX_DEC_CASE(64, 2) RX_DEC_CASE(64, 4) RX_DEC_CASE(64, 8)
+  RX_DEC_CASE(128, 1) RX_DEC_CASE(128, 2) RX_DEC_CASE(128, 4) RX_DEC_CASE(128, 8)
+#undef RX_DEC_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rx

@@ -1,0 +1,407 @@
+// Extend attention (prefill with radix-prefix reuse) on tcgen05 / TMEM (rx_extend).
+//
+// Computes, for request b, new token j (absolute position p = prefix_len + j)
+// and q head h (kv head g = h / G, R14):
+//     o = softmax_{i <= p}(scale * q . K[i]) V[i]
+// where K/V rows 0..prefix_len-1 are the CACHED prefix, read from the pool
+// through rtt ("reduces the computation of prefill"), and
+// rows prefix_len.. are this call's k_new/v_new — which the same launch also
+// stores into their pool slots (A5 fused into A6).
+//
+// B200 design (one CTA per (q tile, kv head, request)):
+//  * M = 128 rows per tile = (128/G tokens) x (G heads of one kv group): GQA
+//    packing makes every K/V tile byte serve G heads (R14);
+//  * warp 0 = TMA producer: Q by a 3-D tiled load; new K/V by 3-D tiled
+//    loads; cached-prefix K/V either by one 3-D tiled load per 64 columns when
+//    the 128 slots of the tile are consecutive (the smallest-first allocator
+//    makes that the common case), or by cp.async.bulk.tensor tile::gather4
+//    (4 pool rows per instruction, issued by all 32 lanes) otherwise; all into
+//    128B-swizzled smem, STAGES-deep ring with full/empty mbarriers;
+//  * warp 1 = single-thread UMMA issuer: S = Q K^T (bf16 -> fp32 TMEM,
+//    double-buffered) then O += P V with P read from TMEM (A operand in
+//    tensor memory), all 128x128 / 128xHD tiles, cta_group::1;
+//  * warps 4-7 = softmax: thread = TMEM lane = row; tcgen05.ld the S row,
+//    causal/length mask, online softmax in the log2 domain with lazy O
+//    rescaling (only when the running max grows by > 8), P packed to bf16 and
+//    tcgen05.st over the S columns; epilogue O / l -> bf16 -> global;
+//  * warps 2-3: TMEM allocation and the fused store of this tile's new K/V
+//    rows into their slots.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "params.cuh"
+#include "ptx.cuh"
+
+namespace rx {
+
+struct ExtendMaps {
+  CUtensorMap q;       // 3D (HD, h_q, N)   box (64, G, TOK)
+  CUtensorMap knew;    // 3D (HD, h_kv, N)  box (64, 1, 128)
+  CUtensorMap vnew;
+  CUtensorMap kpool;   // 3D (HD, h_kv, S)  box (64, 1, 128)
+  CUtensorMap vpool;
+  CUtensorMap kgat;    // 2D (HD, S*h_kv)   box (64, 1)  gather4
+  CUtensorMap vgat;
+};
+
+constexpr int kExtThreads = 256;
+constexpr int kBN = 128;          // kv tokens per tile
+constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
+
+template <int HD>
+struct ExtCfg {
+  static constexpr int NCB = HD / 64;                      // 64-column blocks
+  static constexpr int Q_BYTES = NCB * 128 * kTileRowBytes;
+  static constexpr int KV_BYTES = NCB * kBN * kTileRowBytes;  // one K (or V) tile
+  static constexpr int STAGES = HD == 128 ? 2 : 3;
+  static constexpr int SMEM_DATA = Q_BYTES + STAGES * 2 * KV_BYTES;
+  static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 512;                // S0 | S1 | O
+};
+
+template <int HD, int G>
+__global__ void __launch_bounds__(kExtThreads, 1)
+    extend_kernel(const ExtendParams p, const __grid_constant__ ExtendMaps maps) {
+  using C = ExtCfg<HD>;
+  constexpr int TOK = 128 / G;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);
+  const uint32_t skv = sq + C::Q_BYTES;  // stage s: K at skv + s*2*KV, V at +KV
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;                 // [STAGES]
+  uint64_t* kv_empty = bars + 1 + C::STAGES;    // [STAGES]
+  uint64_t* s_full = bars + 1 + 2 * C::STAGES;  // [2]
+  uint64_t* p_full = s_full + 2;                // [2]
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  const int b = blockIdx.z, g = blockIdx.y;
+  const int t = gridDim.x - 1 - blockIdx.x;  // heaviest (latest) q tiles first
+  const int ext = p.extend_lens[b];
+  if (t * TOK >= ext) return;
+  const int P = p.prefix_lens[b];
+  const int qo = p.qo_indptr[b];
+  const int row = p.rows ? p.rows[b] : b;
+  const int32_t* slots = p.rtt + int64_t(row) * p.rtt_stride;
+  const int rel_end = min(ext, (t + 1) * TOK);
+  const int n_pre = (P + kBN - 1) / kBN;
+  const int n_new = (rel_end + kBN - 1) / kBN;
+  const int n_tiles = n_pre + n_new;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(kv_full + s, 1);
+      mbar_init(kv_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(s_full + s, 1);
+      mbar_init(p_full + s, 128);
+    }
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.q);
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int c = 0; c < C::NCB; ++c)
+        tma_load_3d(sq + c * 128 * kTileRowBytes, &maps.q, q_full, c * 64, g * G, qo + t * TOK);
+    }
+    const int oob_row = int(p.num_slots * p.h_kv);  // coordinate past the end: TMA zero-fills
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j % C::STAGES, rnd = j / C::STAGES;
+      mbar_wait(kv_empty + st, (rnd & 1) ^ 1);
+      const uint32_t kd = skv + st * 2 * C::KV_BYTES, vd = kd + C::KV_BYTES;
+      if (lane == 0) mbar_arrive_expect_tx(kv_full + st, 2 * C::KV_BYTES);
+      __syncwarp();
+      if (j < n_pre) {
+        const int base = j * kBN + 4 * lane;
+        int sl[4];
+        bool contig = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sl[i] = base + i < P ? slots[base + i] : -1;
+        const int s0 = __shfl_sync(0xffffffffu, sl[0], 0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) contig &= (sl[i] == s0 + 4 * lane + i);
+        contig = __all_sync(0xffffffffu, contig);
+        if (contig) {
+          if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < C::NCB; ++c) {
+              tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.kpool, kv_full + st, c * 64, g, s0);
+              tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vpool, kv_full + st, c * 64, g, s0);
+            }
+          }
+        } else {
+          int r[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) r[i] = sl[i] > 0 ? sl[i] * p.h_kv + g : oob_row;
+#pragma unroll
+          for (int c = 0; c < C::NCB; ++c) {
+            const uint32_t off = c * kBN * kTileRowBytes + 4 * lane * kTileRowBytes;
+            tma_gather4(kd + off, &maps.kgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
+            tma_gather4(vd + off, &maps.vgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
+          }
+        }
+      } else if (lane == 0) {
+        const int nn = j - n_pre;
+#pragma unroll
+        for (int c = 0; c < C::NCB; ++c) {
+          tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.knew, kv_full + st, c * 64, g, qo + nn * kBN);
+          tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vnew, kv_full + st, c * 64, g, qo + nn * kBN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
+      const uint32_t t_o = tmem + 256;
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j % C::STAGES;
+        mbar_wait(kv_full + st, (j / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t kb = skv + st * 2 * C::KV_BYTES;
+        const uint32_t t_s = tmem + (j & 1) * 128;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * 128 * kTileRowBytes + (k & 3) * 32;
+          umma_ss(t_s, umma_desc_sw128(sq + off, 16, 1024), umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024),
+                  idesc_s, k > 0);
+        }
+        tc_commit(s_full + (j & 1));
+      };
+      issue_s(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s(j + 1);
+        mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+        tc_fence_after();
+        const int st = j % C::STAGES;
+        const uint32_t vb = skv + st * 2 * C::KV_BYTES + C::KV_BYTES;
+        const uint32_t t_p = tmem + (j & 1) * 128;
+#pragma unroll
+        for (int k = 0; k < kBN / 16; ++k)
+          umma_ts(t_o, t_p + k * 8, umma_desc_sw128(vb + k * 2048, kBN * kTileRowBytes, 1024), idesc_o,
+                  (j > 0 || k > 0) ? 1u : 0u);
+        tc_commit(kv_empty + st);
+        tc_commit(o_done);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int r = (warp - 4) * 32 + lane;          // row = TMEM lane
+    const int i_tok = r / G, h = r % G;
+    const int rel = t * TOK + i_tok;               // position relative to prefix_len
+    const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const uint32_t t_s = tmem + lane_off + (j & 1) * 128;
+      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+      tc_fence_after();
+      float sv[kBN];
+#pragma unroll
+      for (int c = 0; c < kBN / 32; ++c) tmem_ld32(t_s + c * 32, sv + c * 32);
+      tmem_ld_wait();
+      // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel
+      int lim;
+      if (j < n_pre) lim = P - j * kBN - 1;
+      else lim = rel - (j - n_pre) * kBN;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kBN; ++c) {
+        sv[c] = c <= lim ? sv[c] * p.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, sv[c]);
+      }
+      if (mx > m_ref + 8.f || j == 0) {
+        const float m_new = fmaxf(mx, m_ref);
+        const float corr = fast_exp2(m_ref - m_new);
+        if (j > 0) {
+          // O rescale needs the previous P.V to have landed in TMEM
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+          const uint32_t t_o = tmem + lane_off + 256;
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            float ov[32];
+            tmem_ld32(t_o + c * 32, ov);
+            tmem_ld_wait();
+            uint32_t ou[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ou[e] = __float_as_uint(ov[e] * corr);
+            tmem_st32(t_o + c * 32, ou);
+          }
+        }
+        l *= corr;
+        m_ref = m_new;
+      }
+      uint32_t pk[kBN / 2];
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < kBN / 2; ++c) {
+        const float e0 = fast_exp2(sv[2 * c] - m_ref), e1 = fast_exp2(sv[2 * c + 1] - m_ref);
+        rs += e0 + e1;
+        pk[c] = pack_bf16(e0, e1);
+      }
+      l += rs;
+      tmem_st32(t_s, pk);
+      tmem_st32(t_s + 32, pk + 32);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_full + (j & 1));
+    }
+    mbar_wait(o_done, (n_tiles - 1) & 1);
+    tc_fence_after();
+    const uint32_t t_o = tmem + lane_off + 256;
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = p.o + (int64_t(qo + rel) * p.h_q + g * G + h) * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      float ov[32];
+      tmem_ld32(t_o + c * 32, ov);
+      tmem_ld_wait();
+      if (rel < ext) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint4 v;
+          v.x = pack_bf16(ov[8 * e + 0] * inv, ov[8 * e + 1] * inv);
+          v.y = pack_bf16(ov[8 * e + 2] * inv, ov[8 * e + 3] * inv);
+          v.z = pack_bf16(ov[8 * e + 4] * inv, ov[8 * e + 5] * inv);
+          v.w = pack_bf16(ov[8 * e + 6] * inv, ov[8 * e + 7] * inv);
+          dst[e] = v;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ warps 2-3: fused KV store (A5)
+    const int tid = threadIdx.x - 64;              // 0..63
+    const int n_tok = rel_end - t * TOK;
+    constexpr int VPR = HD / 8;                     // 16-byte vectors per head row
+    for (int idx = tid; idx < n_tok * VPR; idx += 64) {
+      const int i = idx / VPR, c = idx % VPR;
+      const int relp = t * TOK + i;
+      const int64_t slot = slots[P + relp];
+      const int64_t src = (int64_t(qo + relp) * p.h_kv + g) * HD + c * 8;
+      const int64_t dst = (slot * p.h_kv + g) * HD + c * 8;
+      *reinterpret_cast<uint4*>(p.kpool + dst) = *reinterpret_cast<const uint4*>(p.k_new + src);
+      *reinterpret_cast<uint4*>(p.vpool + dst) = *reinterpret_cast<const uint4*>(p.v_new + src);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                     const uint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t d[5], s[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int HD, int G>
+static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t total_new, int batch,
+                                   int max_ext, cudaStream_t st) {
+  using C = ExtCfg<HD>;
+  constexpr int TOK = 128 / G;
+  ExtendMaps mp;
+  const uint64_t hd = HD;
+  const uint64_t N = total_new > 0 ? uint64_t(total_new) : 1;
+  {
+    uint64_t dims[3] = {hd, uint64_t(p.h_q), N};
+    uint64_t str[2] = {hd * 2, uint64_t(p.h_q) * hd * 2};
+    uint32_t box[3] = {64, uint32_t(G), uint32_t(TOK)};
+    if (!make_map(&mp.q, q, 3, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    uint64_t dims[3] = {hd, uint64_t(p.h_kv), N};
+    uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
+    uint32_t box[3] = {64, 1, kBN};
+    if (!make_map(&mp.knew, p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.vnew, p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    uint64_t dims[3] = {hd, uint64_t(p.h_kv), uint64_t(p.num_slots)};
+    uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
+    uint32_t box[3] = {64, 1, kBN};
+    if (!make_map(&mp.kpool, p.kpool, 3, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.vpool, p.vpool, 3, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    uint64_t dims[2] = {hd, uint64_t(p.num_slots) * uint64_t(p.h_kv)};
+    uint64_t str[1] = {hd * 2};
+    uint32_t box[2] = {64, 1};
+    if (!make_map(&mp.kgat, p.kpool, 2, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.vgat, p.vpool, 2, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(extend_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  const int qt = (max_ext + TOK - 1) / TOK;
+  dim3 grid(qt, p.h_kv, batch);
+  extend_kernel<HD, G><<<grid, kExtThreads, C::SMEM, st>>>(p, mp);
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void* q, int64_t total_new, int batch,
+                          int max_ext, cudaStream_t st) {
+  if (max_ext <= 0 || batch <= 0) return cudaSuccess;
+#define RX_EXT_CASE(HD_, G_) \
+  if (head_dim == HD_ && G == G_) return launch_extend_t<HD_, G_>(p, q, total_new, batch, max_ext, st);
+  RX_EXT_CASE(64, 1) RX_EXT_CASE(64, 2) RX_EXT_CASE(64, 4) RX_EXT_CASE(64, 8)
+  RX_EXT_CASE(128, 1) RX_EXT_CASE(128, 2) RX_EXT_CASE(128, 4) RX_EXT_CASE(128, 8)
+#undef RX_EXT_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rx

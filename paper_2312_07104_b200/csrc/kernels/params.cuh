@@ -1,0 +1,80 @@
+// Kernel parameter blocks and launcher prototypes shared by the rx kernels
+// and their C-ABI wrappers (attn_api.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace rx {
+
+struct DecodeParams {
+  const __nv_bfloat16* q;       // [B, h_q, HD]
+  const __nv_bfloat16* kpool;   // [S, h_kv, HD]
+  const __nv_bfloat16* vpool;
+  __nv_bfloat16* o;             // [B, h_q, HD]
+  const int32_t* rtt;
+  int64_t rtt_stride;
+  const int32_t* rows;          // nullable
+  const int32_t* seq_lens;      // [B]
+  float* ws_o;                  // [B, h_q, max_splits, HD]
+  float* ws_lse;                // [B, h_q, max_splits]
+  int h_q, h_kv;
+  int chunk;                    // tokens per split (multiple of 16)
+  int max_splits;
+  float scale_log2;             // sm_scale * log2(e)
+};
+
+struct ExtendParams {
+  const int32_t* rtt;
+  int64_t rtt_stride;
+  const int32_t* rows;
+  const int32_t* prefix_lens;
+  const int32_t* extend_lens;
+  const int32_t* qo_indptr;
+  const __nv_bfloat16* k_new;   // [N, h_kv, HD]
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* kpool;         // [S, h_kv, HD]
+  __nv_bfloat16* vpool;
+  __nv_bfloat16* o;             // [N, h_q, HD]
+  int h_q, h_kv;
+  int64_t num_slots;
+  float scale_log2;
+};
+
+struct DecodePlan {
+  int chunk;
+  int max_splits;
+};
+
+// Split-KV plan: a fixed function of (batch, h_kv, max_seq_len) only — NOT of
+// the device's SM count — so a P-GPU run and the same shards run one after
+// another on one GPU partition identically (SURVEY §8(e) "fake TP").
+inline DecodePlan plan_decode(int batch, int h_kv, int max_seq_len) {
+  const int64_t units = int64_t(batch) * h_kv;
+  const int64_t target_ctas = 8 * 148;
+  int64_t chunk = (units * max_seq_len + target_ctas - 1) / target_ctas;
+  chunk = chunk < 256 ? 256 : chunk;
+  chunk = (chunk + 63) / 64 * 64;
+  if (chunk > max_seq_len) chunk = (int64_t(max_seq_len) + 15) / 16 * 16;
+  if (chunk < 16) chunk = 16;
+  const int max_splits = int((max_seq_len + chunk - 1) / chunk);
+  return {int(chunk), max_splits};
+}
+
+inline size_t decode_ws_bytes(int h_q, int head_dim, int batch, int max_seq_len, int h_kv) {
+  DecodePlan pl = plan_decode(batch, h_kv, max_seq_len);
+  if (pl.max_splits <= 1) return 0;
+  const size_t n = size_t(batch) * h_q * pl.max_splits;
+  return n * head_dim * sizeof(float) + n * sizeof(float) + 256;
+}
+
+cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
+                            void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st);
+cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st, int* launches);
+cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void* q, int64_t total_new, int batch,
+                          int max_ext, cudaStream_t st);
+
+}  // namespace rx

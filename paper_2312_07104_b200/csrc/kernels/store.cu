@@ -1,0 +1,47 @@
+// KV store (rx_store_kv): k_pool[slot_i] = k_i, v_pool[slot_i] = v_i, bit-exact,
+// plus the optional req_to_token append rtt_flat[idx_i] = slot_i.
+// "KV cache tensors are stored in a non-contiguous, paged layout, where the
+// size of each page is equivalent to one token" (§3): a token's
+// page is one contiguous pool row of h_kv*head_dim bf16.
+//
+// Pure copy: 16-byte vector loads/stores, one warp per row chunk, grid sized
+// to the row count.  HBM-bound: 2 * row_bytes read + written per token.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "params.cuh"
+
+namespace rx {
+
+__global__ void __launch_bounds__(256) store_kv_kernel(int64_t n, int row_vec, const int32_t* __restrict__ slots,
+                                                       const int4* __restrict__ k, const int4* __restrict__ v,
+                                                       int4* __restrict__ kpool, int4* __restrict__ vpool,
+                                                       int32_t* __restrict__ rtt, const int64_t* __restrict__ rtt_idx) {
+  // one thread per 16-byte vector; row i occupies vectors [i*row_vec, (i+1)*row_vec)
+  const int64_t total = n * row_vec;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / row_vec;
+    const int c = int(t - i * row_vec);
+    const int64_t slot = slots[i];
+    kpool[slot * row_vec + c] = k[t];
+    vpool[slot * row_vec + c] = v[t];
+    if (rtt_idx && c == 0) rtt[rtt_idx[i]] = int32_t(slot);
+  }
+}
+
+cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
+                            void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int row_vec = row_bytes / 16;
+  const int64_t total = n * row_vec;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  store_kv_kernel<<<int(blocks), 256, 0, st>>>(n, row_vec, slots, static_cast<const int4*>(k),
+                                                static_cast<const int4*>(v), static_cast<int4*>(kpool),
+                                                static_cast<int4*>(vpool), rtt, rtt_idx);
+  return cudaPeekAtLastError();
+}
+
+}  // namespace rx

@@ -1,0 +1,388 @@
+"""Request-flow harness over librx (SURVEY §3 "Build, planned"; L4 in SURVEY §1).
+
+Drives one workload (rxgen.workloads C1-C5) through the paper's flow — Alg. 1
+ for batches admitted whole — calling only the C ABI:
+
+  match_prefix -> inc_ref -> alloc (evict shortfall, retry once) ->
+  rx_extend (store new KV + attend) -> decode steps (alloc 1 slot/request,
+  rx_store_kv + rtt append, rx_decode) -> dec_ref -> insert.
+
+Usable prefix is capped at n-1 so every request has a query row (R11).
+
+Two passes:
+  * plan pass (``plan_only=True``): tree ops only; records, per attention
+    call, the prefix hashes of the rows it will process;
+  * execute pass: same tree ops (deterministic, so identical results) plus the
+    kernels, with inputs taken from an ``InputBank`` generated from the plan
+    BEFORE any timing (inputs resident in HBM when timing starts).
+
+Tensor parallelism (§3, "each GPU maintains a sharded KV cache.
+There is no need for additional synchronization because the tree operations
+are the same"): rank r of P owns q heads [r*H_q/P, (r+1)*H_q/P) and the kv
+heads they read; every rank runs the identical tree ops; outputs are
+reassembled by one all_gather per attention call (see ``tp.py``).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from rxgen.hashing import prefix_hashes, next_token, splitmix64_int, MASK64
+from rxgen.values import gen_values, KIND_K, KIND_V, KIND_Q
+
+from . import api
+
+
+class OutOfSlots(RuntimeError):
+    pass
+
+
+def shard_heads(h_q: int, h_kv: int, rank: int, size: int):
+    """(q heads, kv heads) owned by this TP rank; kv heads replicated when size > h_kv."""
+    assert h_q % size == 0, "h_q must divide by the TP size"
+    qh = list(range(rank * h_q // size, (rank + 1) * h_q // size))
+    G = h_q // h_kv
+    kvh = sorted({h // G for h in qh})
+    return qh, kvh
+
+
+class _Req:
+    __slots__ = ("rid", "tokens", "hashes", "n_prompt", "n_out", "node", "prefix", "slots", "row")
+
+    def __init__(self, rid, prompt, n_out, seed, vocab, full=None):
+        self.rid = rid
+        self.n_prompt = len(prompt)
+        self.n_out = n_out
+        if full is None:
+            toks = [int(t) for t in prompt]
+            hs = [int(h) for h in prefix_hashes(toks, seed)]
+            for _ in range(n_out):
+                h = hs[-1]
+                t = next_token(h, vocab)
+                toks.append(t)
+                hs.append(splitmix64_int((h ^ t) & MASK64))
+            full = (toks, hs)
+        self.tokens, self.hashes = full
+        self.node = 0
+        self.prefix = 0
+        self.slots = None
+        self.row = 0
+
+
+@dataclass
+class CallPlan:
+    kind: str                       # "extend" | "decode"
+    hashes: np.ndarray              # uint64 hashes of the rows (query tokens) of the call, packed
+    meta: dict = field(default_factory=dict)
+
+
+class InputBank:
+    """q / k / v of every attention call of a workload, on the device, packed per call."""
+
+    def __init__(self, calls, shape, heads_q, heads_kv, device, q_scale=1.0):
+        self.ext = []
+        self.dec = []
+        hd = shape.head_dim
+        for c in calls:
+            h = c.hashes
+            q = gen_values(h, heads_q, KIND_Q, hd, scale=q_scale, device=device)
+            k = gen_values(h, heads_kv, KIND_K, hd, device=device)
+            v = gen_values(h, heads_kv, KIND_V, hd, device=device)
+            (self.ext if c.kind == "extend" else self.dec).append((q, k, v))
+
+    def nbytes(self):
+        return sum(t.numel() * t.element_size() for lst in (self.ext, self.dec) for tr in lst for t in tr)
+
+
+class Engine:
+    def __init__(self, wl, device="cuda", tp_rank=0, tp_size=1, plan_only=False, record=False,
+                 keep_outputs=False, gather=None):
+        self.wl = wl
+        self.shape = wl.shape
+        self.device = device
+        self.plan_only = plan_only
+        self.record = record
+        self.keep_outputs = keep_outputs
+        self.gather = gather                  # callable(local o) -> full o, or None (P == 1)
+        self.heads_q, self.heads_kv = shard_heads(wl.shape.h_q, wl.shape.h_kv, tp_rank, tp_size)
+        self.hq, self.hkv = len(self.heads_q), len(self.heads_kv)
+        self.cfg = api.attn_cfg(self.hq, self.hkv, wl.shape.head_dim, wl.shape.sm_scale)
+        self.cache = api.RadixCache(wl.num_slots)
+        self.trace = []
+        self.calls = []                      # CallPlan per attention call (plan pass)
+        self.outputs = []                    # (kind, o tensor, meta) per call if keep_outputs
+        self.stats = {"prompt_tokens": 0, "cached_prompt_tokens": 0, "extend_tokens": 0, "decode_tokens": 0,
+                      "tree_s": 0.0, "launches": 0}
+        self._ext_i = 0
+        self._dec_i = 0
+        self.bank = None
+        self._full_cache = {}
+        self.timer = None
+        if not plan_only:
+            hd = wl.shape.head_dim
+            self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
+            self.v_pool = torch.zeros_like(self.k_pool)
+
+    # ------------------------------------------------------------------ tree helpers
+    def _rec(self, *t):
+        if self.record:
+            self.trace.append(t)
+
+    def _alloc(self, n):
+        c = self.cache
+        s = c.rx_alloc(n)
+        if s is None:
+            short = n - c.rx_available()
+            ev, runs = c.rx_evict(short)
+            self._rec("evict", short, ev, tuple(tuple(int(x) for x in r) for r in runs))
+            s = c.rx_alloc(n)
+            if s is None:
+                raise OutOfSlots(f"need {n}, available {c.rx_available()}")
+        if self.record:
+            self._rec("alloc", n, tuple(int(x) for x in s))
+        return s
+
+    # ------------------------------------------------------------------ one batch
+    def run_batch(self, reqs, full_seqs=None):
+        wl = self.wl
+        t0 = time.perf_counter()
+        rs = []
+        for i, q in enumerate(reqs):
+            key = (q.tag, len(q.prompt), q.max_new_tokens)
+            fs = full_seqs[i] if full_seqs is not None else self._full_cache.get(key)
+            r = _Req(q.tag, q.prompt, q.max_new_tokens, wl.seed, wl.vocab, fs)
+            self._full_cache[key] = (r.tokens, r.hashes)
+            rs.append(r)
+        B = len(rs)
+        c = self.cache
+        n_prompt = np.array([r.n_prompt for r in rs], dtype=np.int64)
+        n_out = np.array([r.n_out for r in rs], dtype=np.int64)
+        stride = int((n_prompt + n_out).max())
+        slots = np.zeros((B, stride), dtype=np.int32)        # host mirror of this batch's req_to_token rows
+        prefix = np.empty(B, dtype=np.int64)
+        for b, r in enumerate(rs):                           # match_prefix
+            node, m, sl = c.rx_match_prefix(r.tokens[:r.n_prompt])
+            if self.record:
+                self._rec("match", r.rid, m, tuple(int(x) for x in sl))
+            r.node = node
+            r.prefix = min(m, r.n_prompt - 1)                  # R11
+            prefix[b] = r.prefix
+            slots[b, :r.prefix] = sl[:r.prefix]
+        self.stats["prompt_tokens"] += int(n_prompt.sum())
+        self.stats["cached_prompt_tokens"] += int(prefix.sum())
+        for r in rs:                                           # increase_ref_counter
+            self._rec("inc_ref", r.rid, c.rx_inc_ref(r.node))
+        ext = n_prompt - prefix
+        new = self._alloc(int(ext.sum()))
+        off = 0
+        for b in range(B):
+            slots[b, prefix[b]:n_prompt[b]] = new[off:off + ext[b]]
+            off += ext[b]
+        self.stats["tree_s"] += time.perf_counter() - t0
+        self._slots_host = slots
+        self._extend(rs, slots, prefix, ext)
+        t0 = time.perf_counter()
+        for b, r in enumerate(rs):
+            if r.n_out == 0:
+                self._finish(r, slots[b])
+        running = np.nonzero(n_out > 0)[0]
+        self.stats["tree_s"] += time.perf_counter() - t0
+        step = 0
+        while len(running):
+            t0 = time.perf_counter()
+            new = self._alloc(len(running))
+            pos = n_prompt[running] + step
+            slots[running, pos] = new
+            self.stats["tree_s"] += time.perf_counter() - t0
+            self._decode(rs, running, new, pos)
+            step += 1
+            t0 = time.perf_counter()
+            done = n_out[running] <= step
+            for b in running[done]:
+                self._finish(rs[b], slots[b])
+            running = running[~done]
+            self.stats["tree_s"] += time.perf_counter() - t0
+        self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
+        return rs
+
+    def _finish(self, r: _Req, row_slots):
+        c = self.cache
+        self._rec("dec_ref", r.rid, c.rx_dec_ref(r.node))
+        n = r.n_prompt + r.n_out
+        self._rec("insert", r.rid, *c.rx_insert(r.tokens[:n], row_slots[:n]))
+
+    # ------------------------------------------------------------------ attention calls
+    def _extend(self, rs, slots, prefix, ext):
+        total = int(ext.sum())
+        B = len(rs)
+        self.stats["extend_tokens"] += total
+        if self.plan_only:
+            hs = np.array([h for r in rs for h in r.hashes[r.prefix:r.n_prompt]], dtype=np.uint64)
+            self.calls.append(CallPlan("extend", hs, {"ext": ext.tolist(), "prefix": prefix.tolist()}))
+            return
+        dev = self.device
+        q, k_new, v_new = self.bank.ext[self._ext_i]
+        self._ext_i += 1
+        # one pinned staging block: [prefix | ext | qo_indptr] then the rtt rows
+        stride = slots.shape[1]
+        hdr = 3 * (B + 1)
+        stage = torch.empty(hdr + B * stride, dtype=torch.int32, pin_memory=True)
+        sn = stage.numpy()
+        sn[0:B] = prefix
+        sn[B + 1:2 * B + 1] = ext
+        sn[2 * B + 2] = 0
+        sn[2 * B + 3:3 * B + 3] = np.cumsum(ext)
+        sn[hdr:] = slots.reshape(-1)
+        dstage = stage.to(dev, non_blocking=True)
+        self._stage_keep = stage                  # keep the pinned block alive until the copy lands
+        self._rtt = dstage[hdr:].view(B, stride)
+        self._B = B
+        ws_n = api.rx_decode_workspace_bytes(self.cfg, B, stride)
+        self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
+        self._dec_pin32 = torch.empty((3 * B,), dtype=torch.int32, pin_memory=True)
+        self._dec_pin64 = torch.empty((B,), dtype=torch.int64, pin_memory=True)
+        self._ev = None
+        o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+        ev0 = self._tbeg()
+        api.rx_extend(self.cfg, self._rtt, None, dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
+                      total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o)
+        nl = api.rx_last_launch_count()
+        self.stats["launches"] += nl
+        if ev0 is not None:
+            # algorithmic FLOPs: 4*hd*H_q*sum(n*p + n(n+1)/2), causal-masked work not counted
+            n, p_ = ext.astype(np.float64), prefix.astype(np.float64)
+            flops = 4.0 * self.shape.head_dim * self.hq * float(np.sum(n * p_ + n * (n + 1) / 2))
+            self._tend(ev0, "extend", flops, nl)
+        if self.gather is not None:
+            o = self.gather(o)
+        if self.keep_outputs:
+            self.outputs.append(("extend", o, {"ext": ext.tolist()}))
+
+    def _decode(self, rs, running, new_slots, pos):
+        B = len(running)
+        self.stats["decode_tokens"] += B
+        if self.plan_only:
+            hs = np.array([rs[b].hashes[p] for b, p in zip(running, pos)], dtype=np.uint64)
+            self.calls.append(CallPlan("decode", hs, {"B": B}))
+            return
+        dev = self.device
+        q, k, v = self.bank.dec[self._dec_i]
+        self._dec_i += 1
+        stride = self._rtt.shape[1]
+        if self._ev is not None:
+            self._ev.synchronize()                 # previous step's H2D has consumed the pinned block
+        p32, p64 = self._dec_pin32, self._dec_pin64
+        pn = p32.numpy()[:3 * B].reshape(3, B)     # contiguous prefix of the pinned block
+        pn[0] = new_slots
+        pn[1] = pos + 1                             # seq_len counts the new token
+        pn[2] = running                             # table row of each running request
+        p64.numpy()[:B] = running * stride + pos    # flat req_to_token index of the new token
+        d32 = p32[:3 * B].to(dev, non_blocking=True).view(3, B)
+        d64 = p64[:B].to(dev, non_blocking=True)
+        self._ev = torch.cuda.Event()
+        self._ev.record()
+        ev0 = self._tbeg()
+        api.rx_store_kv(self.cfg, d32[0], k, v, self.k_pool, self.v_pool, self._rtt, d64)
+        launches = api.rx_last_launch_count()
+        if ev0 is not None:
+            self._tend(ev0, "store", 2.0 * 2 * B * self.hkv * self.shape.head_dim * 2, launches)
+            ev0 = self._tbeg()
+        o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+        api.rx_decode(self.cfg, self._rtt, d32[2], d32[1], int(pos.max()) + 1, q, self.k_pool, self.v_pool, o,
+                      self._ws)
+        nl = api.rx_last_launch_count()
+        self.stats["launches"] += launches + nl
+        if ev0 is not None:
+            # algorithmic bytes: unique pool rows read (K+V) + q + o + slot indices;
+            # every running request owns its rows here unless they share a cached prefix node,
+            # so count distinct slots
+            self._tend(ev0, "decode", (self._slots_host, running.copy(), pos.copy()), nl)
+        if self.gather is not None:
+            o = self.gather(o)
+        if self.keep_outputs:
+            self.outputs.append(("decode", o, {"B": B}))
+
+    # ------------------------------------------------------------------ timing hooks
+    def enable_timing(self, on=True):
+        self.timer = [] if on else None
+
+    def _tbeg(self):
+        if self.timer is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def _tend(self, ev0, kind, work, launches):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.timer.append((kind, ev0, e, work, launches))
+
+    def decode_bytes(self, work):
+        """(algorithmic, logical) bytes of one rx_decode call: distinct pool rows read once (K+V),
+        plus q, o and the slot indices; logical counts every request's rows."""
+        slots, running, pos = work
+        hd, B = self.shape.head_dim, len(running)
+        L = int(pos.max()) + 1
+        mask = np.arange(L)[None, :] <= pos[:, None]
+        uniq = np.unique(slots[running][:, :L][mask]).size
+        extra = 2 * B * self.hq * hd * 2 + 4 * int((pos + 1).sum())
+        row = self.hkv * hd * 2 * 2
+        return float(uniq * row + extra), float(int((pos + 1).sum()) * row + extra)
+
+    def timing_summary(self):
+        """{kind: (total ms, launches, calls, total work)} from the recorded events (call after a sync)."""
+        out = {}
+        for kind, a, b, work, nl in self.timer or []:
+            ms = a.elapsed_time(b)
+            t = out.setdefault(kind, [0.0, 0, 0, 0.0])
+            t[0] += ms
+            t[1] += nl
+            t[2] += 1
+            t[3] += self.decode_bytes(work)[0] if kind == "decode" else work
+        return out
+
+    # ------------------------------------------------------------------ workloads
+    def reset(self):
+        """Fresh tree + slot pool for another pass; device pools and the input bank are kept."""
+        self.cache.close()
+        self.cache = api.RadixCache(self.wl.num_slots)
+        self.trace = []
+        self.outputs = []
+        self._ext_i = self._dec_i = 0
+        for k in ("prompt_tokens", "cached_prompt_tokens", "extend_tokens", "decode_tokens", "launches"):
+            self.stats[k] = 0
+        self.stats["tree_s"] = 0.0
+
+    def run_workload(self, bank: InputBank | None = None):
+        if not self.plan_only:
+            assert bank is not None, "execute pass needs an InputBank (build it from a plan pass)"
+            self.bank = bank
+        wl = self.wl
+        if wl.name == "C3":
+            return self._run_chat()
+        for kind, reqs in wl.phases:
+            self.run_batch(reqs)
+        return self
+
+    def _run_chat(self):
+        from rxgen.workloads import Request
+        m = self.wl.meta
+        hist = [np.asarray(m["system"], dtype=np.int32) for _ in m["turn_inputs"]]
+        for t in range(m["turns"]):
+            reqs = [Request(np.concatenate([hist[s], m["turn_inputs"][s][t]]), m["turn_outputs"][s][t], f"s{s}t{t}")
+                    for s in range(len(hist))]
+            done = self.run_batch(reqs)
+            hist = [np.asarray(r.tokens, dtype=np.int32) for r in done]
+        return self
+
+
+def plan_and_bank(wl, device="cuda", tp_rank=0, tp_size=1, q_scale=1.0):
+    """Plan pass + input generation (untimed setup).  Returns (plan engine, InputBank)."""
+    plan = Engine(wl, device=device, tp_rank=tp_rank, tp_size=tp_size, plan_only=True)
+    plan.run_workload()
+    bank = InputBank(plan.calls, wl.shape, plan.heads_q, plan.heads_kv, device, q_scale=q_scale)
+    return plan, bank

@@ -1,0 +1,121 @@
+"""End-to-end GPU parity: whole workloads through librx (C++ tree + kernels via
+the C ABI) against the oracle driver (Python tree + fp64 attention).
+
+* tree trace bit-exact (every matched length, slot vector, eviction run);
+* attention outputs within max-abs 2e-2 / mean-abs 2e-3 on every row for the
+  small configs, and on sampled rows at the full C5 / C3 sizes (the launch
+  configuration bench.py times).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.driver import OracleEngine
+from rxgen import workloads
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2312_07104_b200.engine import Engine, plan_and_bank
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+def _run_gpu(wl, q_scale=1.0):
+    plan, bank = plan_and_bank(wl, "cuda", q_scale=q_scale)
+    e = Engine(wl, "cuda", record=True, keep_outputs=True)
+    e.run_workload(bank)
+    torch.cuda.synchronize()
+    return e
+
+
+def _outputs_by_key(e):
+    """engine outputs -> {("extend", call, req, j) / ("decode", call, req): bf16 row}"""
+    ext = [x for x in e.outputs if x[0] == "extend"]
+    dec = [x for x in e.outputs if x[0] == "decode"]
+    return ext, dec
+
+
+def _compare(o_eng, wl, rows_ext, rows_dec, q_scale=1.0):
+    ext_s = {}
+    dec_s = {}
+
+    def se(call, seqs):
+        return rows_ext(call, seqs)
+
+    def sd(call, step, running):
+        return rows_dec(call, step, running)
+
+    oe = OracleEngine(wl, sample_extend=se, sample_decode=sd, q_scale=q_scale)
+    oe.run_workload()
+    ext, dec = _outputs_by_key(o_eng)
+    errs = []
+    for key, ref in oe.outputs.items():
+        if key[0] == "extend":
+            _, call, bi, j = key
+            o, meta = ext[call][1], ext[call][2]
+            off = int(np.sum(meta["ext"][:bi]))
+            got = o[off + j]
+        else:
+            _, call, bi = key
+            got = dec[call][1][bi]
+        g = got.float().cpu().double().numpy()
+        errs.append(np.abs(g - ref))
+    err = np.concatenate([x.ravel() for x in errs])
+    assert np.isfinite(err).all()
+    assert err.max() <= MAX_ABS, err.max()
+    assert err.mean() <= MEAN_ABS, err.mean()
+    return oe
+
+
+def _all_ext(call, seqs):
+    return [(i, j) for i, s in enumerate(seqs) for j in range(s.n_prompt - s.prefix_len)]
+
+
+def _all_dec(call, step, running):
+    return list(range(len(running)))
+
+
+@pytest.mark.parametrize("q_scale", [1.0, 4.0])
+def test_c1_full_parity(q_scale):
+    wl = workloads.c1()
+    e = _run_gpu(wl, q_scale)
+    oe = _compare(e, wl, _all_ext, _all_dec, q_scale)
+    assert oe.trace == e.trace
+
+
+def test_c2_small_parity():
+    wl = workloads.c2(n_req=6, prefix=300, new_lo=20, new_hi=150, decode=5, num_slots=8192)
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, _all_ext, _all_dec)
+    assert oe.trace == e.trace
+
+
+def test_c3_small_parity():
+    wl = workloads.c3(sessions=5, turns=3, in_lo=20, in_hi=140, out_lo=3, out_hi=20, num_slots=8192)
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, _all_ext, _all_dec)
+    assert oe.trace == e.trace
+
+
+def test_c5_small_parity():
+    wl = workloads.c5(n_req=5, prefix=700, question=40, decode=4, num_slots=8192, ragged=True)
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, _all_ext, _all_dec)
+    assert oe.trace == e.trace
+
+
+def test_c5_full_size_sampled():
+    """BASELINE C5 at full size (8k shared context, batch 128, 32 decode steps): sampled rows."""
+    wl = workloads.c5()
+
+    def re(call, seqs):
+        if call == 0:
+            return [(0, j) for j in (0, 1, 127, 4095, 8190)]
+        return [(i, j) for i in (0, 77, 127) for j in (0, 63, 127)]
+
+    def rd(call, step, running):
+        return [0, 127] if call in (0, 31) else []
+
+    e = _run_gpu(wl)
+    _compare(e, wl, re, rd)

@@ -1,0 +1,239 @@
+"""GPU parity: librx kernels (through the C ABI) against the fp64 oracle.
+
+Tolerance (BASELINE.json north star): max-abs 2e-2 and mean-abs 2e-3 on the
+bf16 outputs vs the oracle's fp64 result; plus relative-error and peaked
+(q x 4) variants (reading R19).  Stores are checked bit-exact.  Inputs are
+rxgen values (seeded, synthetic); slots are deliberately fragmented or
+contiguous to hit both gather paths of the extend kernel, and lengths are
+ragged (tile tails, splits).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as A
+from rxgen.values import gen_values, KIND_K, KIND_V, KIND_Q
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2312_07104_b200 as rx
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+def _vals(rng, n, heads, kind, hd, scale=1.0):
+    h = rng.integers(0, 2**63, n, dtype=np.uint64)
+    return gen_values(h, range(heads), kind, hd, scale=scale)
+
+
+def _cmp(got_bf16, ref64, tag=""):
+    got = got_bf16.float().cpu().double().numpy()
+    err = np.abs(got - ref64)
+    assert np.isfinite(got).all(), tag
+    assert err.max() <= MAX_ABS, f"{tag} max-abs {err.max()}"
+    assert err.mean() <= MEAN_ABS, f"{tag} mean-abs {err.mean()}"
+    return err.max(), err.mean()
+
+
+def _pool(S, h_kv, hd, rng):
+    k = torch.zeros((S, h_kv, hd), dtype=torch.bfloat16)
+    v = torch.zeros_like(k)
+    return k, v
+
+
+def test_store_kv_bit_exact():
+    rng = np.random.default_rng(0)
+    S, h_kv, hd, n = 500, 4, 128, 77
+    cfg = rx.attn_cfg(8, h_kv, hd, 1 / math.sqrt(hd))
+    kp = torch.zeros((S, h_kv, hd), dtype=torch.bfloat16, device="cuda")
+    vp = torch.zeros_like(kp)
+    slots = rng.permutation(np.arange(1, S))[:n].astype(np.int32)
+    k = _vals(rng, n, h_kv, KIND_K, hd).cuda()
+    v = _vals(rng, n, h_kv, KIND_V, hd).cuda()
+    rtt = torch.zeros((4, 64), dtype=torch.int32, device="cuda")
+    idx = torch.from_numpy(rng.permutation(256)[:n].astype(np.int64)).cuda()
+    rx.rx_store_kv(cfg, torch.from_numpy(slots).cuda(), k, v, kp, vp, rtt, idx)
+    torch.cuda.synchronize()
+    assert torch.equal(kp[torch.from_numpy(slots).long().cuda()], k)
+    assert torch.equal(vp[torch.from_numpy(slots).long().cuda()], v)
+    assert torch.equal(rtt.view(-1)[idx], torch.from_numpy(slots).cuda())
+    untouched = np.setdiff1d(np.arange(S), slots)
+    assert kp[torch.from_numpy(untouched).cuda()].abs().sum().item() == 0
+
+
+DEC_CASES = [
+    # (h_q, h_kv, hd, seq_lens)
+    (8, 2, 64, [1, 2, 15, 16, 17, 97, 300]),
+    (32, 32, 128, [1, 5, 64, 129, 1600]),
+    (32, 8, 128, [33, 511, 512, 513, 2000, 4100]),
+    (64, 8, 128, [1, 17, 1000, 8300]),
+    (16, 8, 128, [40, 700]),
+    (8, 8, 64, [3, 1025]),
+]
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,lens", DEC_CASES)
+@pytest.mark.parametrize("q_scale", [1.0, 4.0])
+def test_decode_vs_oracle(h_q, h_kv, hd, lens, q_scale):
+    rng = np.random.default_rng(len(lens) * 7 + hd + h_q)
+    B = len(lens)
+    S = sum(lens) + 64
+    kall = _vals(rng, S, h_kv, KIND_K, hd)
+    vall = _vals(rng, S, h_kv, KIND_V, hd)
+    kall[0] = 0
+    vall[0] = 0
+    stride = max(lens) + 8
+    rtt = np.zeros((B, stride), dtype=np.int32)
+    perm = rng.permutation(np.arange(1, S))
+    off = 0
+    for b, L in enumerate(lens):
+        rtt[b, :L] = perm[off:off + L]     # fragmented slots
+        off += L
+    q = _vals(rng, B, h_q, KIND_Q, hd, scale=q_scale)
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    kp, vp = kall.cuda(), vall.cuda()
+    o = torch.empty((B, h_q, hd), dtype=torch.bfloat16, device="cuda")
+    ws_n = rx.rx_decode_workspace_bytes(cfg, B, max(lens))
+    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device="cuda")
+    rx.rx_decode(cfg, torch.from_numpy(rtt).cuda(), None, torch.tensor(lens, dtype=torch.int32, device="cuda"),
+                 max(lens), q.cuda(), kp, vp, o, ws)
+    torch.cuda.synchronize()
+    pool = A.OraclePool(S, h_kv, hd)
+    pool.store(np.arange(S), kall.float().numpy(), vall.float().numpy())
+    ref = A.decode(pool, [rtt[b] for b in range(B)], lens, q.float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
+    _cmp(o, ref, f"decode {h_q}/{h_kv}/{hd} {lens}")
+    # exact special case: seq_len 1 -> o == v_0 bit for bit
+    for b, L in enumerate(lens):
+        if L == 1:
+            G = h_q // h_kv
+            exp = vall[rtt[b, 0]].repeat_interleave(G, 0)
+            assert torch.equal(o[b].cpu(), exp)
+
+
+def test_decode_rows_indirection():
+    """d_rows selects table rows: permuting rows and seq_lens together permutes outputs."""
+    rng = np.random.default_rng(11)
+    h_q, h_kv, hd = 32, 8, 128
+    lens = [100, 257, 31]
+    S = 1000
+    kp = _vals(rng, S, h_kv, KIND_K, hd).cuda()
+    vp = _vals(rng, S, h_kv, KIND_V, hd).cuda()
+    rtt = torch.from_numpy(rng.integers(1, S, (3, 300)).astype(np.int32)).cuda()
+    q = _vals(rng, 3, h_q, KIND_Q, hd).cuda()
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    o1 = torch.empty((3, h_q, hd), dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, 3, 300) + 1, dtype=torch.uint8, device="cuda")
+    rx.rx_decode(cfg, rtt, None, torch.tensor(lens, dtype=torch.int32, device="cuda"), 257, q, kp, vp, o1, ws)
+    perm = [2, 0, 1]
+    rx.rx_decode(cfg, rtt, torch.tensor(perm, dtype=torch.int32, device="cuda"),
+                 torch.tensor([lens[i] for i in perm], dtype=torch.int32, device="cuda"), 257, q[perm].contiguous(),
+                 kp, vp, o2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(o2, o1[perm])
+
+
+EXT_CASES = [
+    # (h_q, h_kv, hd, prefix_lens, extend_lens, contiguous_prefix)
+    (8, 2, 64, [64] * 4, [32] * 4, True),
+    (8, 2, 64, [0, 1, 63, 200], [1, 5, 33, 130], False),
+    (32, 32, 128, [0, 128, 129], [128, 1, 200], True),
+    (32, 32, 128, [300, 17], [129, 64], False),
+    (32, 8, 128, [0, 256, 511], [300, 17, 130], False),
+    (32, 8, 128, [384, 384], [100, 256], True),
+    (64, 8, 128, [1000, 0], [40, 150], True),
+    (64, 8, 128, [257, 513], [16, 17], False),
+    (16, 8, 128, [10, 140], [140, 10], False),
+]
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,pre,ext,contig", EXT_CASES)
+@pytest.mark.parametrize("q_scale", [1.0, 4.0])
+def test_extend_vs_oracle(h_q, h_kv, hd, pre, ext, contig, q_scale):
+    rng = np.random.default_rng(sum(pre) + sum(ext) + hd)
+    B = len(pre)
+    S = sum(pre) + sum(ext) + 300
+    stride = max(p + e for p, e in zip(pre, ext)) + 3
+    rtt = np.zeros((B, stride), dtype=np.int32)
+    free = list(range(1, S)) if contig else list(rng.permutation(np.arange(1, S)))
+    off = 0
+    for b in range(B):
+        n = pre[b] + ext[b]
+        rtt[b, :n] = free[off:off + n]
+        off += n
+    kpool = _vals(rng, S, h_kv, KIND_K, hd)
+    vpool = _vals(rng, S, h_kv, KIND_V, hd)
+    N = sum(ext)
+    q = _vals(rng, N, h_q, KIND_Q, hd, scale=q_scale)
+    kn = _vals(rng, N, h_kv, KIND_K, hd)
+    vn = _vals(rng, N, h_kv, KIND_V, hd)
+    indptr = np.concatenate([[0], np.cumsum(ext)]).astype(np.int32)
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    kp, vp = kpool.cuda(), vpool.cuda()
+    o = torch.full((N, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    rx.rx_extend(cfg, torch.from_numpy(rtt).cuda(), None, torch.tensor(pre, dtype=torch.int32, device="cuda"),
+                 torch.tensor(ext, dtype=torch.int32, device="cuda"), torch.from_numpy(indptr).cuda(), N, max(ext),
+                 max(pre), q.cuda(), kn.cuda(), vn.cuda(), kp, vp, o)
+    torch.cuda.synchronize()
+    pool = A.OraclePool(S, h_kv, hd)
+    pool.store(np.arange(S), kpool.float().numpy(), vpool.float().numpy())
+    ref = A.extend(pool, [rtt[b] for b in range(B)], pre, ext, q.float().numpy(), kn.float().numpy(),
+                   vn.float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
+    _cmp(o, ref, f"extend {h_q}/{h_kv}/{hd} pre={pre} ext={ext}")
+    # fused store: new rows landed in their slots bit-exact, prefix rows untouched
+    for b in range(B):
+        s_new = torch.from_numpy(rtt[b, pre[b]:pre[b] + ext[b]].astype(np.int64)).cuda()
+        assert torch.equal(kp[s_new], kn[indptr[b]:indptr[b + 1]].cuda())
+        assert torch.equal(vp[s_new], vn[indptr[b]:indptr[b + 1]].cuda())
+        s_pre = torch.from_numpy(rtt[b, :pre[b]].astype(np.int64)).cuda()
+        assert torch.equal(kp[s_pre], kpool[rtt[b, :pre[b]].astype(np.int64)].cuda())
+
+
+def test_extend_decode_consistency():
+    """decode(seq_lens) == extend(prefix = seq_len - 1, n = 1) within tolerance of each other."""
+    rng = np.random.default_rng(3)
+    h_q, h_kv, hd = 32, 8, 128
+    lens = [1, 130, 700]
+    B = len(lens)
+    S = 2000
+    kpool = _vals(rng, S, h_kv, KIND_K, hd).cuda()
+    vpool = _vals(rng, S, h_kv, KIND_V, hd).cuda()
+    rtt = np.zeros((B, 800), dtype=np.int32)
+    off = 1
+    for b, L in enumerate(lens):
+        rtt[b, :L] = np.arange(off, off + L)
+        off += L
+    rtt_d = torch.from_numpy(rtt).cuda()
+    q = _vals(rng, B, h_q, KIND_Q, hd).cuda()
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    od = torch.empty((B, h_q, hd), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, 800) + 1, dtype=torch.uint8, device="cuda")
+    rx.rx_decode(cfg, rtt_d, None, torch.tensor(lens, dtype=torch.int32, device="cuda"), 700, q, kpool, vpool, od, ws)
+    last = torch.from_numpy(np.array([rtt[b, L - 1] for b, L in enumerate(lens)], dtype=np.int64)).cuda()
+    oe = torch.empty_like(od)
+    rx.rx_extend(cfg, rtt_d, None, torch.tensor([L - 1 for L in lens], dtype=torch.int32, device="cuda"),
+                 torch.ones(B, dtype=torch.int32, device="cuda"), torch.arange(B + 1, dtype=torch.int32, device="cuda"),
+                 B, 1, max(lens) - 1, q, kpool[last].contiguous(), vpool[last].contiguous(), kpool.clone(),
+                 vpool.clone(), oe)
+    torch.cuda.synchronize()
+    assert (od.float() - oe.float()).abs().max().item() < 2e-2
+
+
+def test_unsupported_and_invalid():
+    cfg = rx.attn_cfg(12, 4, 128, 0.1)                  # G = 3
+    o = torch.empty((1, 12, 128), dtype=torch.bfloat16, device="cuda")
+    z = torch.zeros((4, 4, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(rx.RxError) as e:
+        rx.rx_decode(cfg, torch.zeros((1, 4), dtype=torch.int32, device="cuda"), None,
+                     torch.ones(1, dtype=torch.int32, device="cuda"), 1, o, z, z, o)
+    assert e.value.status == -5
+    cfg = rx.attn_cfg(8, 2, 96, 0.1)
+    with pytest.raises(rx.RxError):
+        rx.rx_decode(cfg, torch.zeros((1, 4), dtype=torch.int32, device="cuda"), None,
+                     torch.ones(1, dtype=torch.int32, device="cuda"), 1, o, z, z, o)
+    with pytest.raises(ValueError):
+        rx.rx_decode(rx.attn_cfg(8, 2, 64, 0.1), torch.zeros((1, 4), dtype=torch.int32), None,
+                     torch.ones(1, dtype=torch.int32), 1, o, z, z, o)
