@@ -134,25 +134,66 @@ class OracleEngine:
         new_cached, dup = self.tree.insert(seq.tokens, seq.slots)
         self.trace.append(("insert", seq.rid, new_cached, dup))
 
-    def run_batch(self, reqs, rids=None):
-        """Run one admitted batch to completion; returns the finished Seqs (with full tokens)."""
-        wl = self.wl
-        seqs = []
-        for i, r in enumerate(reqs):
-            rid = rids[i] if rids is not None else r.tag
-            seqs.append(Seq(rid, r.prompt, r.max_new_tokens, wl.seed, wl.vocab))
-        # 1. match_prefix (P:526-528); usable prefix capped at n-1 (R11)
+    def _match(self, seqs):
+        """Alg. 1 "for req in requests: T.match_prefix"; usable prefix capped at n-1 (R11)."""
         for s in seqs:
-            node, m, slots = self.tree.match_prefix(s.tokens)
+            node, m, slots = self.tree.match_prefix(s.tokens[:s.n_prompt])
             self.trace.append(("match", s.rid, m, tuple(slots)))
             s.node = node
+            s.matched = m
             s.prefix_len = min(m, s.n_prompt - 1)
             s.slots = list(slots[:s.prefix_len])
-            self.stats["prompt_tokens"] += s.n_prompt
-            self.stats["cached_prompt_tokens"] += s.prefix_len
-        # 2. increase_ref_counter (P:541)
+
+    def _seqs(self, reqs):
+        return [Seq(r.tag, r.prompt, r.max_new_tokens, self.wl.seed, self.wl.vocab) for r in reqs]
+
+    def run_batch(self, reqs):
+        """Run one batch admitted whole: match, pin, then run to completion."""
+        seqs = self._seqs(reqs)
+        self._match(seqs)
         for s in seqs:
             self.trace.append(("inc_ref", s.rid, self.tree.inc_ref(s.node)))
+        return self._run_matched(seqs)
+
+    def run_waves(self, reqs):
+        """Alg. 1 admission repeated until every request has run.
+
+        Each wave: match every waiting request, sort by matched length
+        (longest first, ties by arrival), admit while req.size() + current <
+        available with available = evictable + free updated by the
+        inc_ref delta and current += req.size() (R7); req.size()
+        = new prompt tokens + max_new_tokens.  The admitted batch runs to
+        completion (reading R22: waves instead of per-iteration joins)."""
+        waiting = self._seqs(reqs)
+        done = []
+        while waiting:
+            self._match(waiting)
+            order = sorted(range(len(waiting)), key=lambda i: (-waiting[i].matched, i))
+            available = self.tree.evictable_size() + self.tree.available()
+            current = 0
+            admitted = []
+            for i in order:
+                s = waiting[i]
+                size = (s.n_prompt - s.prefix_len) + s.n_out
+                if size + current < available:
+                    d = self.tree.inc_ref(s.node)
+                    self.trace.append(("inc_ref", s.rid, d))
+                    available += d
+                    current += size
+                    admitted.append(i)
+            if not admitted:
+                raise OOM("no waiting request fits the pool")
+            self.trace.append(("admit", tuple(waiting[i].rid for i in admitted)))
+            done.extend(self._run_matched([waiting[i] for i in admitted]))
+            keep = set(admitted)
+            waiting = [s for i, s in enumerate(waiting) if i not in keep]
+        by_rid = {s.rid: s for s in done}
+        return [by_rid[r.tag] for r in reqs]
+
+    def _run_matched(self, seqs):
+        for s in seqs:
+            self.stats["prompt_tokens"] += s.n_prompt
+            self.stats["cached_prompt_tokens"] += s.prefix_len
         # 3. alloc with evict-retry (P:551-556)
         ext = [s.n_prompt - s.prefix_len for s in seqs]
         new = self._alloc(sum(ext))
@@ -205,6 +246,8 @@ class OracleEngine:
         wl = self.wl
         if wl.name == "C3":
             return self._run_chat()
+        if wl.name == "C4":
+            return self._run_tot()
         for kind, reqs in wl.phases:
             self.run_batch(reqs)
         return self
@@ -218,4 +261,15 @@ class OracleEngine:
                     for s in range(len(hist))]
             done = self.run_batch(reqs)
             hist = [np.asarray(d.tokens, dtype=np.int32) for d in done]
+        return self
+
+    def _run_tot(self):
+        """C4: tree-of-thought; root as a hint, then each level's branches under Alg. 1 admission."""
+        from rxgen.workloads import Request
+        m = self.wl.meta
+        self.run_batch([Request(np.asarray(m["root"], dtype=np.int32), 0, "root")])
+        parents = [np.asarray(m["root"], dtype=np.int32)]
+        for lvl, nodes in enumerate(m["levels"]):
+            reqs = [Request(np.concatenate([parents[p], bp]), tl, f"L{lvl}n{i}") for i, (p, bp, tl) in enumerate(nodes)]
+            parents = [np.asarray(s.tokens, dtype=np.int32) for s in self.run_waves(reqs)]
         return self

@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   uint64_t* s_full = bars + 1 + 2 * C::STAGES;  // [2]
   uint64_t* p_full = s_full + 2;                // [2]
   uint64_t* o_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* o_final = o_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int b = blockIdx.z, g = blockIdx.y;
   const int t = gridDim.x - 1 - blockIdx.x;  // heaviest (latest) q tiles first
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(p_full + s, 128);
     }
     mbar_init(o_done, 1);
+    mbar_init(o_final, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         tc_commit(kv_empty + st);
         tc_commit(o_done);
       }
+      tc_commit(o_final);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
@@ -231,11 +234,17 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         sv[c] = c <= lim ? sv[c] * p.scale_log2 : -INFINITY;
         mx = fmaxf(mx, sv[c]);
       }
-      if (mx > m_ref + 8.f || j == 0) {
+      // Lazy rescale, decided per WARP: tcgen05.ld/st are .sync.aligned
+      // warp-collective, so the O round trip must not diverge across rows.
+      // Lanes whose max did not grow get corr = 1.
+      if (__any_sync(0xffffffffu, mx > m_ref + 8.f) || j == 0) {
         const float m_new = fmaxf(mx, m_ref);
         const float corr = fast_exp2(m_ref - m_new);
         if (j > 0) {
           // O rescale needs the previous P.V to have landed in TMEM
+          // o_done completes once per P.V.  Having seen S_j complete, and since a
+          // tcgen05.commit tracks ALL prior MMAs of the issuer, P.V_{j-2} is done:
+          // completions are j-1 or j, so the parity wait for P.V_{j-1} is exact.
           mbar_wait(o_done, (j - 1) & 1);
           tc_fence_after();
           const uint32_t t_o = tmem + lane_off + 256;
@@ -268,7 +277,9 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       tc_fence_before();
       mbar_arrive(p_full + (j & 1));
     }
-    mbar_wait(o_done, (n_tiles - 1) & 1);
+    // up to two P.V may still be in flight here: wait on the one-shot barrier
+    // committed after the last one instead of an ambiguous o_done parity
+    mbar_wait(o_final, 0);
     tc_fence_after();
     const uint32_t t_o = tmem + lane_off + 256;
     const float inv = 1.f / l;

@@ -50,7 +50,7 @@ def shard_heads(h_q: int, h_kv: int, rank: int, size: int):
 
 
 class _Req:
-    __slots__ = ("rid", "tokens", "hashes", "n_prompt", "n_out", "node", "prefix", "slots", "row")
+    __slots__ = ("rid", "tokens", "hashes", "n_prompt", "n_out", "node", "prefix", "slots", "row", "matched")
 
     def __init__(self, rid, prompt, n_out, seed, vocab, full=None):
         self.rid = rid
@@ -146,35 +146,87 @@ class Engine:
         return s
 
     # ------------------------------------------------------------------ one batch
-    def run_batch(self, reqs, full_seqs=None):
+    def _reqs(self, reqs):
         wl = self.wl
-        t0 = time.perf_counter()
         rs = []
-        for i, q in enumerate(reqs):
+        for q in reqs:
             key = (q.tag, len(q.prompt), q.max_new_tokens)
-            fs = full_seqs[i] if full_seqs is not None else self._full_cache.get(key)
-            r = _Req(q.tag, q.prompt, q.max_new_tokens, wl.seed, wl.vocab, fs)
+            r = _Req(q.tag, q.prompt, q.max_new_tokens, wl.seed, wl.vocab, self._full_cache.get(key))
             self._full_cache[key] = (r.tokens, r.hashes)
             rs.append(r)
+        return rs
+
+    def _match(self, rs):
+        """match_prefix for every request (Alg. 1); usable prefix capped at n-1 (R11)."""
+        c = self.cache
+        for r in rs:
+            node, m, sl = c.rx_match_prefix(r.tokens[:r.n_prompt])
+            if self.record:
+                self._rec("match", r.rid, m, tuple(int(x) for x in sl))
+            r.node = node
+            r.matched = m
+            r.prefix = min(m, r.n_prompt - 1)
+            r.slots = sl[:r.prefix]
+
+    def run_batch(self, reqs):
+        """One batch admitted whole: match, pin every request, run to completion."""
+        t0 = time.perf_counter()
+        rs = self._reqs(reqs)
+        self._match(rs)
+        for r in rs:
+            d = self.cache.rx_inc_ref(r.node)
+            self._rec("inc_ref", r.rid, d)
+        self.stats["tree_s"] += time.perf_counter() - t0
+        return self._run_matched(rs)
+
+    def run_waves(self, reqs):
+        """Alg. 1 admission (R7) repeated until every request ran (waves, R22).
+
+        Sort by matched length (longest first, ties by arrival); admit while
+        size + current < available, available = evictable + free updated by
+        the inc_ref delta, current += size, size = new prompt tokens + max_new."""
+        c = self.cache
+        waiting = self._reqs(reqs)
+        done = {}
+        while waiting:
+            t0 = time.perf_counter()
+            self._match(waiting)
+            order = sorted(range(len(waiting)), key=lambda i: (-waiting[i].matched, i))
+            available = c.rx_evictable_size() + c.rx_available()
+            current = 0
+            admitted = []
+            for i in order:
+                r = waiting[i]
+                size = (r.n_prompt - r.prefix) + r.n_out
+                if size + current < available:
+                    d = c.rx_inc_ref(r.node)
+                    self._rec("inc_ref", r.rid, d)
+                    available += d
+                    current += size
+                    admitted.append(i)
+            if not admitted:
+                raise OutOfSlots("no waiting request fits the pool")
+            self._rec("admit", tuple(waiting[i].rid for i in admitted))
+            self.stats["tree_s"] += time.perf_counter() - t0
+            for r in self._run_matched([waiting[i] for i in admitted]):
+                done[r.rid] = r
+            keep = set(admitted)
+            waiting = [r for i, r in enumerate(waiting) if i not in keep]
+        return [done[q.tag] for q in reqs]
+
+    def _run_matched(self, rs):
+        t0 = time.perf_counter()
         B = len(rs)
         c = self.cache
         n_prompt = np.array([r.n_prompt for r in rs], dtype=np.int64)
         n_out = np.array([r.n_out for r in rs], dtype=np.int64)
         stride = int((n_prompt + n_out).max())
         slots = np.zeros((B, stride), dtype=np.int32)        # host mirror of this batch's req_to_token rows
-        prefix = np.empty(B, dtype=np.int64)
-        for b, r in enumerate(rs):                           # match_prefix
-            node, m, sl = c.rx_match_prefix(r.tokens[:r.n_prompt])
-            if self.record:
-                self._rec("match", r.rid, m, tuple(int(x) for x in sl))
-            r.node = node
-            r.prefix = min(m, r.n_prompt - 1)                  # R11
-            prefix[b] = r.prefix
-            slots[b, :r.prefix] = sl[:r.prefix]
+        prefix = np.array([r.prefix for r in rs], dtype=np.int64)
+        for b, r in enumerate(rs):
+            slots[b, :r.prefix] = r.slots
         self.stats["prompt_tokens"] += int(n_prompt.sum())
         self.stats["cached_prompt_tokens"] += int(prefix.sum())
-        for r in rs:                                           # increase_ref_counter
-            self._rec("inc_ref", r.rid, c.rx_inc_ref(r.node))
         ext = n_prompt - prefix
         new = self._alloc(int(ext.sum()))                      # P:551-556
         off = 0
@@ -364,6 +416,8 @@ class Engine:
         wl = self.wl
         if wl.name == "C3":
             return self._run_chat()
+        if wl.name == "C4":
+            return self._run_tot()
         for kind, reqs in wl.phases:
             self.run_batch(reqs)
         return self
@@ -377,6 +431,18 @@ class Engine:
                     for s in range(len(hist))]
             done = self.run_batch(reqs)
             hist = [np.asarray(r.tokens, dtype=np.int32) for r in done]
+        return self
+
+    def _run_tot(self):
+        """C4 tree-of-thought: root as a hint, then each level's branches under Alg. 1 admission."""
+        from rxgen.workloads import Request
+        m = self.wl.meta
+        root = np.asarray(m["root"], dtype=np.int32)
+        self.run_batch([Request(root, 0, "root")])
+        parents = [root]
+        for lvl, nodes in enumerate(m["levels"]):
+            reqs = [Request(np.concatenate([parents[p], bp]), tl, f"L{lvl}n{i}") for i, (p, bp, tl) in enumerate(nodes)]
+            parents = [np.asarray(r.tokens, dtype=np.int32) for r in self.run_waves(reqs)]
         return self
 
 

@@ -30,6 +30,8 @@ def _cmp(a, b):
     lambda: workloads.c2(n_req=12, prefix=200, new_lo=5, new_hi=40, decode=6, num_slots=8192),
     lambda: workloads.c3(sessions=10, turns=3, in_lo=5, in_hi=30, out_lo=3, out_hi=12, num_slots=8192),
     lambda: workloads.c5(n_req=8, prefix=300, question=20, decode=5, num_slots=8192),
+    lambda: workloads.c4(),
+    lambda: workloads.c4(seed=1, root=300, p_lo=8, p_hi=40, t_lo=4, t_hi=20, capacity_frac=0.5),
 ])
 def test_trace_equal(cfg):
     o, e = _traces(cfg())
@@ -77,3 +79,12 @@ def test_shard_heads():
     assert shard_heads(64, 8, 1, 2) == (list(range(32, 64)), [4, 5, 6, 7])
     assert shard_heads(8, 2, 3, 4) == ([6, 7], [1])
     assert shard_heads(32, 32, 1, 4) == (list(range(8, 16)), list(range(8, 16)))
+
+
+def test_c4_admission_waves_and_eviction():
+    """C4 at 60% capacity: the deepest level cannot run in one wave (Alg. 1 fit
+    check) and finished branches are evicted LRU to make room."""
+    o, e = _traces(workloads.c4())
+    admits = [t for t in o if t[0] == "admit"]
+    assert len(admits) > 3 and sum(t[0] == "evict" for t in o) > 0
+    _cmp(o, e)
