@@ -205,7 +205,8 @@ rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
  *       [qo_indptr[b], qo_indptr[b+1])
  *   total_new        = qo_indptr[batch] (host copy, sizes the TMA views)
  *   max_extend_len   = max extend_len (host copy, sizes the grid)
- *   max_prefix_len   = max prefix_len (host copy)
+ *   max_prefix_len   = max prefix_len (host copy); rtt_stride must be >= every
+ *       prefix_len + extend_len (only the maxima are checked)
  * Workspace: d_ws of ws_bytes >= rx_extend_workspace_bytes(...). */
 rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch,
                     const int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,

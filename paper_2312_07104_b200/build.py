@@ -23,7 +23,7 @@ LIB = os.path.join(HERE, "librx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Wno-deprecated-gpu-targets", "-I", os.path.join(ROOT, "include")]
 CU_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr"]
 
 

@@ -126,7 +126,7 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
   if (!d_rtt || !d_prefix_lens || !d_extend_lens || !d_qo_indptr || !d_q || !d_k_new || !d_v_new || !d_k_pool ||
       !d_v_pool || !d_o)
     return RX_E_INVALID;
-  if (rtt_stride < int64_t(max_prefix_len) + max_extend_len) return RX_E_INVALID;
+  if (rtt_stride < max_prefix_len || rtt_stride < max_extend_len) return RX_E_INVALID;
   rx::ExtendParams p{};
   p.rtt = d_rtt;
   p.rtt_stride = rtt_stride;

@@ -23,6 +23,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "params.cuh"
 #include "ptx.cuh"
@@ -32,11 +33,11 @@ namespace rx {
 constexpr int kDecWarps = 4;
 constexpr int kBlk = 16;
 
-template <int HD>
+template <int HD, int STAGES_ = (HD == 128 ? 3 : 6)>
 struct DecCfg {
   static constexpr int RB = HD * 2;                   // bytes per row
   static constexpr int BLK_BYTES = kBlk * RB;         // one K (or V) block
-  static constexpr int STAGES = HD == 128 ? 4 : 6;
+  static constexpr int STAGES = STAGES_;
   static constexpr int WARP_BYTES = STAGES * 2 * BLK_BYTES;
   static constexpr int SMEM = kDecWarps * WARP_BYTES;
   static constexpr int CHUNKS = kBlk * HD / 8;        // 16-byte chunks per block
@@ -61,9 +62,9 @@ __device__ __forceinline__ void dec_issue_block(uint32_t kdst, uint32_t vdst, co
   }
 }
 
-template <int HD, int G>
-__global__ void __launch_bounds__(kDecWarps * 32) decode_kernel(const DecodeParams p) {
-  using C = DecCfg<HD>;
+template <int HD, int G, int STAGES>
+__global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeParams p) {
+  using C = DecCfg<HD, STAGES>;
   extern __shared__ __align__(128) uint8_t smem[];
   const int b = blockIdx.z, g = blockIdx.y, s = blockIdx.x;
   const int L = p.seq_lens[b];
@@ -252,16 +253,16 @@ __global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p)
   }
 }
 
-template <int HD, int G>
+template <int HD, int G, int STAGES>
 static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_t st, int* launches) {
-  using C = DecCfg<HD>;
+  using C = DecCfg<HD, STAGES>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(decode_kernel<HD, G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
   dim3 grid(p.max_splits, p.h_kv, batch);
-  decode_kernel<HD, G><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);
+  decode_kernel<HD, G, STAGES><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);
   *launches = 1;
   if (p.max_splits > 1) {
     decode_merge_kernel<HD><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
@@ -270,10 +271,28 @@ static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_
   return cudaPeekAtLastError();
 }
 
+// Pipeline depth per warp: 3 (default: 96 KB smem, 2 CTAs/SM) or 4 (128 KB, 1 CTA/SM)
+// for head_dim 128.  RX_DECODE_STAGES overrides it (development A/B knob).
+static int decode_stages() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RX_DECODE_STAGES");
+    v = e ? atoi(e) : 3;
+    if (v != 2 && v != 3 && v != 4) v = 3;
+  }
+  return v;
+}
+
 cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st,
                           int* launches) {
-#define RX_DEC_CASE(HD_, G_) \
-  if (head_dim == HD_ && G == G_) return launch_decode_t<HD_, G_>(p, batch, st, launches);
+  const int stg = decode_stages();
+#define RX_DEC_CASE(HD_, G_)                                                                  \
+  if (head_dim == HD_ && G == G_) {                                                           \
+    if (HD_ == 64) return launch_decode_t<HD_, G_, 6>(p, batch, st, launches);                \
+    if (stg == 2) return launch_decode_t<HD_, G_, 2>(p, batch, st, launches);                 \
+    if (stg == 4) return launch_decode_t<HD_, G_, 4>(p, batch, st, launches);                 \
+    return launch_decode_t<HD_, G_, 3>(p, batch, st, launches);                               \
+  }
   RX_DEC_CASE(64, 1) RX_DEC_CASE(64, 2) RX_DEC_CASE(64, 4) RX_DEC_CASE(64, 8)
   RX_DEC_CASE(128, 1) RX_DEC_CASE(128, 2) RX_DEC_CASE(128, 4) RX_DEC_CASE(128, 8)
 #undef RX_DEC_CASE

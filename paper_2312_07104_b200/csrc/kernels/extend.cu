@@ -54,14 +54,42 @@ constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
 
 template <int HD>
 struct ExtCfg {
-  static constexpr int NCB = HD / 64;                      // 64-column blocks
-  static constexpr int Q_BYTES = NCB * 128 * kTileRowBytes;
+  static constexpr int NCB = HD / 64;                         // 64-column blocks
+  static constexpr int Q_BYTES = NCB * 128 * kTileRowBytes;   // one Q tile (double-buffered)
   static constexpr int KV_BYTES = NCB * kBN * kTileRowBytes;  // one K (or V) tile
   static constexpr int STAGES = HD == 128 ? 2 : 3;
-  static constexpr int SMEM_DATA = Q_BYTES + STAGES * 2 * KV_BYTES;
-  static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t TMEM_COLS = 512;                // S0 | S1 | O
+  static constexpr int SMEM_DATA = 2 * Q_BYTES + STAGES * 2 * KV_BYTES;
+  static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 512;                  // S0 | S1 | O0 | O1
+  static constexpr uint32_t O_COL = 256;                      // O buffer b at O_COL + b*HD
 };
+
+// One work item = (q tile t, kv head g, request b).  Items are enumerated
+// heaviest first (largest t first: causal work grows with t) and dealt to the
+// persistent CTAs round-robin; every role of a CTA walks the same list.
+struct ExtItem {
+  int b, g, t, P, ext, qo, n_pre, n_tiles;
+  const int32_t* slots;
+};
+
+template <int TOK>
+__device__ __forceinline__ bool ext_item(const ExtendParams& p, int qt, int w, ExtItem& it) {
+  const int per_t = p.h_kv * p.batch;
+  it.t = qt - 1 - w / per_t;
+  const int rem = w % per_t;
+  it.g = rem % p.h_kv;
+  it.b = rem / p.h_kv;
+  it.ext = p.extend_lens[it.b];
+  if (it.t * TOK >= it.ext) return false;
+  it.P = p.prefix_lens[it.b];
+  it.qo = p.qo_indptr[it.b];
+  const int row = p.rows ? p.rows[it.b] : it.b;
+  it.slots = p.rtt + int64_t(row) * p.rtt_stride;
+  const int rel_end = min(it.ext, (it.t + 1) * TOK);
+  it.n_pre = (it.P + kBN - 1) / kBN;
+  it.n_tiles = it.n_pre + (rel_end + kBN - 1) / kBN;
+  return true;
+}
 
 template <int HD, int G>
 __global__ void __launch_bounds__(kExtThreads, 1)
@@ -70,45 +98,38 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   constexpr int TOK = 128 / G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sq = smem_u32(smem);
-  const uint32_t skv = sq + C::Q_BYTES;  // stage s: K at skv + s*2*KV, V at +KV
+  const uint32_t sq = smem_u32(smem);                 // Q buffer qb at sq + qb*Q_BYTES
+  const uint32_t skv = sq + 2 * C::Q_BYTES;           // stage s: K at skv + s*2*KV, V at +KV
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;                 // [STAGES]
-  uint64_t* kv_empty = bars + 1 + C::STAGES;    // [STAGES]
-  uint64_t* s_full = bars + 1 + 2 * C::STAGES;  // [2]
-  uint64_t* p_full = s_full + 2;                // [2]
-  uint64_t* o_done = p_full + 2;
-  uint64_t* o_final = o_done + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
+  uint64_t* q_full = bars;                            // [2]
+  uint64_t* q_empty = bars + 2;                       // [2]
+  uint64_t* kv_full = bars + 4;                       // [STAGES]
+  uint64_t* kv_empty = kv_full + C::STAGES;           // [STAGES]
+  uint64_t* s_full = kv_empty + C::STAGES;            // [2]
+  uint64_t* p_full = s_full + 2;                      // [2]
+  uint64_t* o_done = p_full + 2;                      // one phase per P.V
+  uint64_t* o_ready = o_done + 1;                     // [2] one phase per item (its last P.V)
+  uint64_t* o_free = o_ready + 2;                     // [2] epilogue has read O[b]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
-  const int b = blockIdx.z, g = blockIdx.y;
-  const int t = gridDim.x - 1 - blockIdx.x;  // heaviest (latest) q tiles first
-  const int ext = p.extend_lens[b];
-  if (t * TOK >= ext) return;
-  const int P = p.prefix_lens[b];
-  const int qo = p.qo_indptr[b];
-  const int row = p.rows ? p.rows[b] : b;
-  const int32_t* slots = p.rtt + int64_t(row) * p.rtt_stride;
-  const int rel_end = min(ext, (t + 1) * TOK);
-  const int n_pre = (P + kBN - 1) / kBN;
-  const int n_new = (rel_end + kBN - 1) / kBN;
-  const int n_tiles = n_pre + n_new;
-
+  const int qt = p.max_qtiles;
+  const int W = qt * p.h_kv * p.batch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_ready + i, 1);
+      mbar_init(o_free + i, 128);
+    }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(kv_full + s, 1);
       mbar_init(kv_empty + s, 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(s_full + s, 1);
-      mbar_init(p_full + s, 128);
-    }
     mbar_init(o_done, 1);
-    mbar_init(o_final, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -121,200 +142,238 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       tma_prefetch_desc(&maps.q);
-      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-      for (int c = 0; c < C::NCB; ++c)
-        tma_load_3d(sq + c * 128 * kTileRowBytes, &maps.q, q_full, c * 64, g * G, qo + t * TOK);
+      tma_prefetch_desc(&maps.knew);
+      tma_prefetch_desc(&maps.kpool);
+      tma_prefetch_desc(&maps.kgat);
     }
     const int oob_row = int(p.num_slots * p.h_kv);  // coordinate past the end: TMA zero-fills
-    for (int j = 0; j < n_tiles; ++j) {
-      const int st = j % C::STAGES, rnd = j / C::STAGES;
-      mbar_wait(kv_empty + st, (rnd & 1) ^ 1);
-      const uint32_t kd = skv + st * 2 * C::KV_BYTES, vd = kd + C::KV_BYTES;
-      if (lane == 0) mbar_arrive_expect_tx(kv_full + st, 2 * C::KV_BYTES);
-      __syncwarp();
-      if (j < n_pre) {
-        const int base = j * kBN + 4 * lane;
-        int sl[4];
-        bool contig = true;
+    int it = 0, jg = 0;
+    ExtItem I;
+    for (int w = blockIdx.x; w < W; w += gridDim.x) {
+      if (!ext_item<TOK>(p, qt, w, I)) continue;
+      const int qb = it & 1;
+      if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(q_full + qb, C::Q_BYTES);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) sl[i] = base + i < P ? slots[base + i] : -1;
-        const int s0 = __shfl_sync(0xffffffffu, sl[0], 0);
+        for (int c = 0; c < C::NCB; ++c)
+          tma_load_3d(sq + qb * C::Q_BYTES + c * 128 * kTileRowBytes, &maps.q, q_full + qb, c * 64, I.g * G,
+                      I.qo + I.t * TOK);
+      }
+      for (int j = 0; j < I.n_tiles; ++j, ++jg) {
+        const int st = jg % C::STAGES, rnd = jg / C::STAGES;
+        mbar_wait(kv_empty + st, (rnd & 1) ^ 1);
+        const uint32_t kd = skv + st * 2 * C::KV_BYTES, vd = kd + C::KV_BYTES;
+        if (lane == 0) mbar_arrive_expect_tx(kv_full + st, 2 * C::KV_BYTES);
+        __syncwarp();
+        if (j < I.n_pre) {
+          const int base = j * kBN + 4 * lane;
+          int sl[4];
+          bool contig = true;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) contig &= (sl[i] == s0 + 4 * lane + i);
-        contig = __all_sync(0xffffffffu, contig);
-        if (contig) {
-          if (lane == 0) {
+          for (int i = 0; i < 4; ++i) sl[i] = base + i < I.P ? I.slots[base + i] : -1;
+          const int s0 = __shfl_sync(0xffffffffu, sl[0], 0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) contig &= (sl[i] == s0 + 4 * lane + i);
+          contig = __all_sync(0xffffffffu, contig);
+          if (contig) {
+            if (lane == 0) {
+#pragma unroll
+              for (int c = 0; c < C::NCB; ++c) {
+                tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.kpool, kv_full + st, c * 64, I.g, s0);
+                tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vpool, kv_full + st, c * 64, I.g, s0);
+              }
+            }
+          } else {
+            int r[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r[i] = sl[i] > 0 ? sl[i] * p.h_kv + I.g : oob_row;
 #pragma unroll
             for (int c = 0; c < C::NCB; ++c) {
-              tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.kpool, kv_full + st, c * 64, g, s0);
-              tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vpool, kv_full + st, c * 64, g, s0);
+              const uint32_t off = c * kBN * kTileRowBytes + 4 * lane * kTileRowBytes;
+              tma_gather4(kd + off, &maps.kgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
+              tma_gather4(vd + off, &maps.vgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
             }
           }
-        } else {
-          int r[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) r[i] = sl[i] > 0 ? sl[i] * p.h_kv + g : oob_row;
+        } else if (lane == 0) {
+          const int nn = j - I.n_pre;
 #pragma unroll
           for (int c = 0; c < C::NCB; ++c) {
-            const uint32_t off = c * kBN * kTileRowBytes + 4 * lane * kTileRowBytes;
-            tma_gather4(kd + off, &maps.kgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
-            tma_gather4(vd + off, &maps.vgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
+            tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.knew, kv_full + st, c * 64, I.g, I.qo + nn * kBN);
+            tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vnew, kv_full + st, c * 64, I.g, I.qo + nn * kBN);
           }
         }
-      } else if (lane == 0) {
-        const int nn = j - n_pre;
-#pragma unroll
-        for (int c = 0; c < C::NCB; ++c) {
-          tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.knew, kv_full + st, c * 64, g, qo + nn * kBN);
-          tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vnew, kv_full + st, c * 64, g, qo + nn * kBN);
-        }
       }
+      ++it;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
-      const uint32_t t_o = tmem + 256;
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j % C::STAGES;
-        mbar_wait(kv_full + st, (j / C::STAGES) & 1);
-        tc_fence_after();
-        const uint32_t kb = skv + st * 2 * C::KV_BYTES;
-        const uint32_t t_s = tmem + (j & 1) * 128;
+      int it = 0, jg = 0;
+      ExtItem I;
+      for (int w = blockIdx.x; w < W; w += gridDim.x) {
+        if (!ext_item<TOK>(p, qt, w, I)) continue;
+        const int qb = it & 1;
+        const uint32_t qa = sq + qb * C::Q_BYTES;
+        const uint32_t t_o = tmem + C::O_COL + qb * HD;
+        mbar_wait(q_full + qb, (it >> 1) & 1);
+        if (it >= 2) mbar_wait(o_free + qb, ((it >> 1) - 1) & 1);  // epilogue of item it-2 read O[qb]
+        auto issue_s = [&](int j) {
+          const int g_ = jg + j;
+          const int st = g_ % C::STAGES;
+          mbar_wait(kv_full + st, (g_ / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t kb = skv + st * 2 * C::KV_BYTES;
+          const uint32_t t_s = tmem + (g_ & 1) * 128;
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t off = (k >> 2) * 128 * kTileRowBytes + (k & 3) * 32;
-          umma_ss(t_s, umma_desc_sw128(sq + off, 16, 1024), umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024),
-                  idesc_s, k > 0);
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint32_t off = (k >> 2) * 128 * kTileRowBytes + (k & 3) * 32;
+            umma_ss(t_s, umma_desc_sw128(qa + off, 16, 1024),
+                    umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
+          }
+          tc_commit(s_full + (g_ & 1));
+          if (j == I.n_tiles - 1) tc_commit(q_empty + qb);  // last read of this Q buffer issued
+        };
+        issue_s(0);
+        for (int j = 0; j < I.n_tiles; ++j) {
+          if (j + 1 < I.n_tiles) issue_s(j + 1);
+          const int g_ = jg + j;
+          mbar_wait(p_full + (g_ & 1), (g_ >> 1) & 1);
+          tc_fence_after();
+          const int st = g_ % C::STAGES;
+          const uint32_t vb = skv + st * 2 * C::KV_BYTES + C::KV_BYTES;
+          const uint32_t t_p = tmem + (g_ & 1) * 128;
+#pragma unroll
+          for (int k = 0; k < kBN / 16; ++k)
+            umma_ts(t_o, t_p + k * 8, umma_desc_sw128(vb + k * 2048, kBN * kTileRowBytes, 1024), idesc_o,
+                    (j > 0 || k > 0) ? 1u : 0u);
+          tc_commit(kv_empty + st);
+          tc_commit(o_done);
         }
-        tc_commit(s_full + (j & 1));
-      };
-      issue_s(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s(j + 1);
-        mbar_wait(p_full + (j & 1), (j >> 1) & 1);
-        tc_fence_after();
-        const int st = j % C::STAGES;
-        const uint32_t vb = skv + st * 2 * C::KV_BYTES + C::KV_BYTES;
-        const uint32_t t_p = tmem + (j & 1) * 128;
-#pragma unroll
-        for (int k = 0; k < kBN / 16; ++k)
-          umma_ts(t_o, t_p + k * 8, umma_desc_sw128(vb + k * 2048, kBN * kTileRowBytes, 1024), idesc_o,
-                  (j > 0 || k > 0) ? 1u : 0u);
-        tc_commit(kv_empty + st);
-        tc_commit(o_done);
+        tc_commit(o_ready + qb);
+        jg += I.n_tiles;
+        ++it;
       }
-      tc_commit(o_final);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
     const int r = (warp - 4) * 32 + lane;          // row = TMEM lane
     const int i_tok = r / G, h = r % G;
-    const int rel = t * TOK + i_tok;               // position relative to prefix_len
     const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      const uint32_t t_s = tmem + lane_off + (j & 1) * 128;
-      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
-      tc_fence_after();
-      float sv[kBN];
+    int it = 0, jg = 0;
+    ExtItem I;
+    for (int w = blockIdx.x; w < W; w += gridDim.x) {
+      if (!ext_item<TOK>(p, qt, w, I)) continue;
+      const int qb = it & 1;
+      const int rel = I.t * TOK + i_tok;           // position relative to prefix_len
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < I.n_tiles; ++j) {
+        const int g_ = jg + j;
+        const uint32_t t_s = tmem + lane_off + (g_ & 1) * 128;
+        mbar_wait(s_full + (g_ & 1), (g_ >> 1) & 1);
+        tc_fence_after();
+        float sv[kBN];
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) tmem_ld32(t_s + c * 32, sv + c * 32);
-      tmem_ld_wait();
-      // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel
-      int lim;
-      if (j < n_pre) lim = P - j * kBN - 1;
-      else lim = rel - (j - n_pre) * kBN;
-      float mx = -INFINITY;
+        for (int c = 0; c < kBN / 32; ++c) tmem_ld32(t_s + c * 32, sv + c * 32);
+        tmem_ld_wait();
+        // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel
+        const int lim = j < I.n_pre ? I.P - j * kBN - 1 : rel - (j - I.n_pre) * kBN;
+        float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kBN; ++c) {
-        sv[c] = c <= lim ? sv[c] * p.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, sv[c]);
+        for (int c = 0; c < kBN; ++c) {
+          sv[c] = c <= lim ? sv[c] * p.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, sv[c]);
+        }
+        // Lazy rescale, decided per WARP: tcgen05.ld/st are .sync.aligned
+        // warp-collective, so the O round trip must not diverge across rows.
+        // Lanes whose max did not grow get corr = 1.
+        if (__any_sync(0xffffffffu, mx > m_ref + 8.f) || j == 0) {
+          const float m_new = fmaxf(mx, m_ref);
+          const float corr = fast_exp2(m_ref - m_new);
+          if (j > 0) {
+            // o_done completes once per P.V.  Having seen S_g complete, and since a
+            // tcgen05.commit tracks ALL prior MMAs of the issuer, P.V_{g-2} is done:
+            // completions are g-1 or g, so the parity wait for P.V_{g-1} is exact.
+            mbar_wait(o_done, (g_ - 1) & 1);
+            tc_fence_after();
+            const uint32_t t_o = tmem + lane_off + C::O_COL + qb * HD;
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+              float ov[32];
+              tmem_ld32(t_o + c * 32, ov);
+              tmem_ld_wait();
+              uint32_t ou[32];
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ou[e] = __float_as_uint(ov[e] * corr);
+              tmem_st32(t_o + c * 32, ou);
+            }
+          }
+          l *= corr;
+          m_ref = m_new;
+        }
+        uint32_t pk[kBN / 2];
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < kBN / 2; ++c) {
+          const float e0 = fast_exp2(sv[2 * c] - m_ref), e1 = fast_exp2(sv[2 * c + 1] - m_ref);
+          rs += e0 + e1;
+          pk[c] = pack_bf16(e0, e1);
+        }
+        l += rs;
+        tmem_st32(t_s, pk);
+        tmem_st32(t_s + 32, pk + 32);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full + (g_ & 1));
       }
-      // Lazy rescale, decided per WARP: tcgen05.ld/st are .sync.aligned
-      // warp-collective, so the O round trip must not diverge across rows.
-      // Lanes whose max did not grow get corr = 1.
-      if (__any_sync(0xffffffffu, mx > m_ref + 8.f) || j == 0) {
-        const float m_new = fmaxf(mx, m_ref);
-        const float corr = fast_exp2(m_ref - m_new);
-        if (j > 0) {
-          // O rescale needs the previous P.V to have landed in TMEM
-          // o_done completes once per P.V.  Having seen S_j complete, and since a
-          // tcgen05.commit tracks ALL prior MMAs of the issuer, P.V_{j-2} is done:
-          // completions are j-1 or j, so the parity wait for P.V_{j-1} is exact.
-          mbar_wait(o_done, (j - 1) & 1);
-          tc_fence_after();
-          const uint32_t t_o = tmem + lane_off + 256;
+      // epilogue: O[qb] complete once this item's last P.V landed
+      mbar_wait(o_ready + qb, (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_o = tmem + lane_off + C::O_COL + qb * HD;
+      const float inv = 1.f / l;
+      __nv_bfloat16* orow = p.o + (int64_t(I.qo + rel) * p.h_q + I.g * G + h) * HD;
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
-            float ov[32];
-            tmem_ld32(t_o + c * 32, ov);
-            tmem_ld_wait();
-            uint32_t ou[32];
+      for (int c = 0; c < HD / 32; ++c) {
+        float ov[32];
+        tmem_ld32(t_o + c * 32, ov);
+        tmem_ld_wait();
+        if (rel < I.ext) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) ou[e] = __float_as_uint(ov[e] * corr);
-            tmem_st32(t_o + c * 32, ou);
+          for (int e = 0; e < 4; ++e) {
+            uint4 v;
+            v.x = pack_bf16(ov[8 * e + 0] * inv, ov[8 * e + 1] * inv);
+            v.y = pack_bf16(ov[8 * e + 2] * inv, ov[8 * e + 3] * inv);
+            v.z = pack_bf16(ov[8 * e + 4] * inv, ov[8 * e + 5] * inv);
+            v.w = pack_bf16(ov[8 * e + 6] * inv, ov[8 * e + 7] * inv);
+            dst[e] = v;
           }
         }
-        l *= corr;
-        m_ref = m_new;
       }
-      uint32_t pk[kBN / 2];
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < kBN / 2; ++c) {
-        const float e0 = fast_exp2(sv[2 * c] - m_ref), e1 = fast_exp2(sv[2 * c + 1] - m_ref);
-        rs += e0 + e1;
-        pk[c] = pack_bf16(e0, e1);
-      }
-      l += rs;
-      tmem_st32(t_s, pk);
-      tmem_st32(t_s + 32, pk + 32);
-      tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(p_full + (j & 1));
-    }
-    // up to two P.V may still be in flight here: wait on the one-shot barrier
-    // committed after the last one instead of an ambiguous o_done parity
-    mbar_wait(o_final, 0);
-    tc_fence_after();
-    const uint32_t t_o = tmem + lane_off + 256;
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = p.o + (int64_t(qo + rel) * p.h_q + g * G + h) * HD;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      float ov[32];
-      tmem_ld32(t_o + c * 32, ov);
-      tmem_ld_wait();
-      if (rel < ext) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint4 v;
-          v.x = pack_bf16(ov[8 * e + 0] * inv, ov[8 * e + 1] * inv);
-          v.y = pack_bf16(ov[8 * e + 2] * inv, ov[8 * e + 3] * inv);
-          v.z = pack_bf16(ov[8 * e + 4] * inv, ov[8 * e + 5] * inv);
-          v.w = pack_bf16(ov[8 * e + 6] * inv, ov[8 * e + 7] * inv);
-          dst[e] = v;
-        }
-      }
+      mbar_arrive(o_free + qb);
+      jg += I.n_tiles;
+      ++it;
     }
   } else {
     // ------------------------------------------------------------ warps 2-3: fused KV store (A5)
     const int tid = threadIdx.x - 64;              // 0..63
-    const int n_tok = rel_end - t * TOK;
     constexpr int VPR = HD / 8;                     // 16-byte vectors per head row
-    for (int idx = tid; idx < n_tok * VPR; idx += 64) {
-      const int i = idx / VPR, c = idx % VPR;
-      const int relp = t * TOK + i;
-      const int64_t slot = slots[P + relp];
-      const int64_t src = (int64_t(qo + relp) * p.h_kv + g) * HD + c * 8;
-      const int64_t dst = (slot * p.h_kv + g) * HD + c * 8;
-      *reinterpret_cast<uint4*>(p.kpool + dst) = *reinterpret_cast<const uint4*>(p.k_new + src);
-      *reinterpret_cast<uint4*>(p.vpool + dst) = *reinterpret_cast<const uint4*>(p.v_new + src);
+    ExtItem I;
+    for (int w = blockIdx.x; w < W; w += gridDim.x) {
+      if (!ext_item<TOK>(p, qt, w, I)) continue;
+      const int n_tok = min(I.ext, (I.t + 1) * TOK) - I.t * TOK;
+      for (int idx = tid; idx < n_tok * VPR; idx += 64) {
+        const int i = idx / VPR, c = idx % VPR;
+        const int relp = I.t * TOK + i;
+        const int64_t slot = I.slots[I.P + relp];
+        const int64_t src = (int64_t(I.qo + relp) * p.h_kv + I.g) * HD + c * 8;
+        const int64_t dst = (slot * p.h_kv + I.g) * HD + c * 8;
+        *reinterpret_cast<uint4*>(p.kpool + dst) = *reinterpret_cast<const uint4*>(p.k_new + src);
+        *reinterpret_cast<uint4*>(p.vpool + dst) = *reinterpret_cast<const uint4*>(p.v_new + src);
+      }
     }
   }
   tc_fence_before();
@@ -398,9 +457,18 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
     cudaFuncSetAttribute(extend_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  const int qt = (max_ext + TOK - 1) / TOK;
-  dim3 grid(qt, p.h_kv, batch);
-  extend_kernel<HD, G><<<grid, kExtThreads, C::SMEM, st>>>(p, mp);
+  ExtendParams pp = p;
+  pp.batch = batch;
+  pp.max_qtiles = (max_ext + TOK - 1) / TOK;
+  const int64_t items = int64_t(pp.max_qtiles) * p.h_kv * batch;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = int(items < sms ? items : sms);   // persistent: one CTA per SM
+  extend_kernel<HD, G><<<grid, kExtThreads, C::SMEM, st>>>(pp, mp);
   return cudaPeekAtLastError();
 }
 

@@ -42,6 +42,8 @@ struct ExtendParams {
   int h_q, h_kv;
   int64_t num_slots;
   float scale_log2;
+  int batch;                    // set by the launcher
+  int max_qtiles;               // set by the launcher
 };
 
 struct DecodePlan {

@@ -343,6 +343,9 @@ class Engine:
             self._tend(ev0, "store", 2.0 * 2 * B * self.hkv * self.shape.head_dim * 2, launches)
             ev0 = self._tbeg()
         o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+        need = api.rx_decode_workspace_bytes(self.cfg, B, int(pos.max()) + 1)
+        if need > self._ws.numel():            # split count depends on (B, max_seq): grow on demand
+            self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
         api.rx_decode(self.cfg, self._rtt, d32[2], d32[1], int(pos.max()) + 1, q, self.k_pool, self.v_pool, o,
                       self._ws)
         nl = api.rx_last_launch_count()

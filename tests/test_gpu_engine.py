@@ -46,7 +46,8 @@ def _compare(o_eng, wl, rows_ext, rows_dec, q_scale=1.0):
     def sd(call, step, running):
         return rows_dec(call, step, running)
 
-    oe = OracleEngine(wl, sample_extend=se, sample_decode=sd, q_scale=q_scale)
+    small = wl.num_slots * wl.shape.h_kv * wl.shape.head_dim <= (1 << 26)
+    oe = OracleEngine(wl, sample_extend=se, sample_decode=sd, q_scale=q_scale, materialize=small)
     oe.run_workload()
     ext, dec = _outputs_by_key(o_eng)
     errs = []
@@ -119,3 +120,15 @@ def test_c5_full_size_sampled():
 
     e = _run_gpu(wl)
     _compare(e, wl, re, rd)
+
+
+def test_c4_tot_full_parity():
+    """C4 at full size: tree-of-thought under Alg. 1 admission with the pool at
+    60% of the tree's distinct tokens (evictions between waves)."""
+    wl = workloads.c4()
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, lambda c, seqs: [(i, j) for i, s in enumerate(seqs)
+                                          for j in range(s.n_prompt - s.prefix_len) if j % 7 == 0 or c > 0],
+                  _all_dec)
+    assert oe.trace == e.trace
+    assert any(t[0] == "evict" for t in e.trace)

@@ -237,3 +237,42 @@ def test_unsupported_and_invalid():
     with pytest.raises(ValueError):
         rx.rx_decode(rx.attn_cfg(8, 2, 64, 0.1), torch.zeros((1, 4), dtype=torch.int32), None,
                      torch.ones(1, dtype=torch.int32), 1, o, z, z, o)
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd", [(32, 8, 128), (64, 8, 128), (32, 32, 128), (8, 2, 64)])
+def test_extend_many_items_ragged(h_q, h_kv, hd):
+    """Many (q tile, head, request) items per persistent CTA, ragged lengths, mixed
+    contiguous / fragmented prefixes; peaked softmax (q x 4) to exercise O rescaling."""
+    rng = np.random.default_rng(h_q * 7 + hd)
+    B = 24
+    pre = [int(x) for x in rng.integers(0, 700, B)]
+    pre[0], pre[1] = 0, 128
+    ext = [int(x) for x in rng.integers(1, 300, B)]
+    S = sum(pre) + sum(ext) + 64
+    stride = max(p + e for p, e in zip(pre, ext))
+    rtt = np.zeros((B, stride), dtype=np.int32)
+    order = np.concatenate([np.arange(1, S // 2), rng.permutation(np.arange(S // 2, S))])
+    off = 0
+    for b in range(B):
+        n = pre[b] + ext[b]
+        rtt[b, :n] = order[off:off + n]
+        off += n
+    kpool = _vals(rng, S, h_kv, KIND_K, hd)
+    vpool = _vals(rng, S, h_kv, KIND_V, hd)
+    N = sum(ext)
+    q = _vals(rng, N, h_q, KIND_Q, hd, scale=4.0)
+    kn = _vals(rng, N, h_kv, KIND_K, hd)
+    vn = _vals(rng, N, h_kv, KIND_V, hd)
+    indptr = np.concatenate([[0], np.cumsum(ext)]).astype(np.int32)
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    kp, vp = kpool.cuda(), vpool.cuda()
+    o = torch.full((N, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    rx.rx_extend(cfg, torch.from_numpy(rtt).cuda(), None, torch.tensor(pre, dtype=torch.int32, device="cuda"),
+                 torch.tensor(ext, dtype=torch.int32, device="cuda"), torch.from_numpy(indptr).cuda(), N, max(ext),
+                 max(pre), q.cuda(), kn.cuda(), vn.cuda(), kp, vp, o)
+    torch.cuda.synchronize()
+    pool = A.OraclePool(S, h_kv, hd)
+    pool.store(np.arange(S), kpool.float().numpy(), vpool.float().numpy())
+    ref = A.extend(pool, [rtt[b] for b in range(B)], pre, ext, q.float().numpy(), kn.float().numpy(),
+                   vn.float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
+    _cmp(o, ref, f"extend-many {h_q}/{h_kv}/{hd}")
