@@ -233,6 +233,20 @@ rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch,
                     const void* d_q, const void* d_k_pool, const void* d_v_pool,
                     int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Decode step with the newest token's KV appended in the same launch (A4 + A5
+ * + A7 + A8): for every request b, k_new[b] / v_new[b] ([batch, h_kv,
+ * head_dim] bf16) are stored into pool slot new_slots[b] (int32 [batch],
+ * device), rtt[row_b][seq_len[b] - 1] = new_slots[b] is recorded, and the
+ * query attends over positions 0 .. seq_len[b]-1 including the new token.
+ * Equivalent to rx_store_kv(...) followed by rx_decode(...), in one kernel
+ * (plus the split merge).  d_rtt is written (one entry per request). */
+rx_status rx_decode_append(const rx_attn_cfg* cfg, int32_t batch,
+                           int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
+                           const int32_t* d_seq_lens, int32_t max_seq_len,
+                           const void* d_q, const void* d_k_new, const void* d_v_new,
+                           const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
+                           int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream);
+
 size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len);
 
 /* Number of kernel launches the last successful rx_extend / rx_decode /

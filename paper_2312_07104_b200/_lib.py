@@ -53,6 +53,8 @@ SIGNATURES = {
                             vp, vp, vp, vp, vp, i64, vp, vp, sz, vp]),
     "rx_extend_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
     "rx_decode": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, i64, vp, vp, sz, vp]),
+    "rx_decode_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, i64,
+                                   vp, vp, sz, vp]),
     "rx_decode_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
     "rx_last_launch_count": (i32, []),
 }

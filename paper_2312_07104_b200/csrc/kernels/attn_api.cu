@@ -64,10 +64,11 @@ size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t 
   return rx::decode_ws_bytes(cfg->h_q, cfg->head_dim, batch, max_seq_len, cfg->h_kv);
 }
 
-rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
-                    const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
-                    const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
-                    size_t ws_bytes, void* stream) {
+static rx_status decode_impl(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
+                             const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
+                             const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
+                             size_t ws_bytes, void* stream, const void* d_k_new, const void* d_v_new,
+                             const int32_t* d_new_slots, int32_t* d_rtt_w) {
   rx_status s = check_cfg(cfg);
   if (s != RX_OK) return s;
   if (batch < 0 || max_seq_len < 0 || num_slots < 1) return RX_E_INVALID;
@@ -95,12 +96,33 @@ rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
   p.chunk = pl.chunk;
   p.max_splits = pl.max_splits;
   p.scale_log2 = cfg->sm_scale * 1.4426950408889634f;
+  p.k_new = static_cast<const __nv_bfloat16*>(d_k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(d_v_new);
+  p.new_slots = d_new_slots;
+  p.rtt_w = d_rtt_w;
   int launches = 0;
   cudaError_t e = rx::launch_decode(cfg->head_dim, cfg->h_q / cfg->h_kv, p, batch,
                                     static_cast<cudaStream_t>(stream), &launches);
   if (e != cudaSuccess) return RX_E_CUDA;
   g_last_launches = launches;
   return RX_OK;
+}
+
+rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
+                    const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
+                    const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
+                    size_t ws_bytes, void* stream) {
+  return decode_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_pool, d_v_pool,
+                     num_slots, d_o, d_ws, ws_bytes, stream, nullptr, nullptr, nullptr, nullptr);
+}
+
+rx_status rx_decode_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
+                           const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
+                           const void* d_k_new, const void* d_v_new, const int32_t* d_new_slots, void* d_k_pool,
+                           void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_k_new || !d_v_new || !d_new_slots) return RX_E_INVALID;
+  return decode_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_pool, d_v_pool,
+                     num_slots, d_o, d_ws, ws_bytes, stream, d_k_new, d_v_new, d_new_slots, d_rtt);
 }
 
 size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len) {

@@ -75,6 +75,27 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   const int row = p.rows ? p.rows[b] : b;
   const int32_t* slots = p.rtt + int64_t(row) * p.rtt_stride;
 
+  // Decode-append (rx_decode_append): the newest token's KV arrives with the
+  // call.  The last split of each (request, kv head) stores that head's row
+  // into the pool slot (A5) and, for kv head 0, appends the slot to the
+  // req_to_token row (A4); position L-1 then reads its slot from the argument,
+  // never from the table, so no CTA races the table write.
+  const bool append = p.new_slots != nullptr;
+  const int new_slot = append ? p.new_slots[b] : 0;
+  if (append && s == nsplit - 1) {
+    constexpr int VPR = HD / 8;                      // 16-byte vectors per head row
+    const int64_t src = (int64_t(b) * p.h_kv + g) * HD;
+    const int64_t dst = (int64_t(new_slot) * p.h_kv + g) * HD;
+    if (threadIdx.x < VPR)
+      reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.kpool) + dst)[threadIdx.x] =
+          reinterpret_cast<const uint4*>(p.k_new + src)[threadIdx.x];
+    else if (threadIdx.x < 2 * VPR)
+      reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.vpool) + dst)[threadIdx.x - VPR] =
+          reinterpret_cast<const uint4*>(p.v_new + src)[threadIdx.x - VPR];
+    if (g == 0 && threadIdx.x == 2 * VPR) p.rtt_w[int64_t(row) * p.rtt_stride + L - 1] = new_slot;
+    __syncthreads();  // the row is in L2 before this CTA's cp.async gathers read it
+  }
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
 
@@ -103,7 +124,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   auto load_slot = [&](int i) -> int {
     if (i >= my || lane >= kBlk) return 0;
     const int t = tok0(i) + lane;
-    return t < end ? slots[t] : 0;
+    return t < end ? ((append && t == L - 1) ? new_slot : slots[t]) : 0;
   };
 
 #pragma unroll

@@ -25,6 +25,12 @@ struct DecodeParams {
   int chunk;                    // tokens per split (multiple of 16)
   int max_splits;
   float scale_log2;             // sm_scale * log2(e)
+  // decode-append (nullable): newest token's K/V [B, h_kv, HD] and slot [B];
+  // rtt_w is the writable view of rtt for the append
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  const int32_t* new_slots;
+  int32_t* rtt_w;
 };
 
 struct ExtendParams {

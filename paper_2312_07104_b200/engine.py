@@ -294,9 +294,12 @@ class Engine:
         self._B = B
         ws_n = api.rx_decode_workspace_bytes(self.cfg, B, stride)
         self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
-        self._dec_pin32 = torch.empty((3 * B,), dtype=torch.int32, pin_memory=True)
-        self._dec_pin64 = torch.empty((B,), dtype=torch.int64, pin_memory=True)
-        self._ev = None
+        # decode-step staging: two pinned blocks [new_slots | seq_lens | rows] (host may run 2 steps ahead)
+        self._dec_pin = [torch.empty((3 * B,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self._dec_dev = torch.empty((2, 3 * B), dtype=torch.int32, device=dev)
+        self._dec_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self._dec_used = [False, False]
+        self._dec_n = 0
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         ev0 = self._tbeg()
         api.rx_extend(self.cfg, self._rtt, None, dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
@@ -323,37 +326,32 @@ class Engine:
         dev = self.device
         q, k, v = self.bank.dec[self._dec_i]
         self._dec_i += 1
-        stride = self._rtt.shape[1]
-        if self._ev is not None:
-            self._ev.synchronize()                 # previous step's H2D has consumed the pinned block
-        p32, p64 = self._dec_pin32, self._dec_pin64
-        pn = p32.numpy()[:3 * B].reshape(3, B)     # contiguous prefix of the pinned block
-        pn[0] = new_slots
-        pn[1] = pos + 1                             # seq_len counts the new token
-        pn[2] = running                             # table row of each running request
-        p64.numpy()[:B] = running * stride + pos    # flat req_to_token index of the new token
-        d32 = p32[:3 * B].to(dev, non_blocking=True).view(3, B)
-        d64 = p64[:B].to(dev, non_blocking=True)
-        self._ev = torch.cuda.Event()
-        self._ev.record()
-        ev0 = self._tbeg()
-        api.rx_store_kv(self.cfg, d32[0], k, v, self.k_pool, self.v_pool, self._rtt, d64)
-        launches = api.rx_last_launch_count()
-        if ev0 is not None:
-            self._tend(ev0, "store", 2.0 * 2 * B * self.hkv * self.shape.head_dim * 2, launches)
-            ev0 = self._tbeg()
+        i = self._dec_n & 1
+        self._dec_n += 1
+        if self._dec_used[i]:
+            self._dec_ev[i].synchronize()           # the H2D copy from two steps ago consumed this block
+        pin = self._dec_pin[i]
+        pn = pin.numpy()
+        pn[0:B] = new_slots
+        pn[B:2 * B] = pos + 1                       # seq_len counts the new token
+        pn[2 * B:3 * B] = running                   # table row of each running request
+        d = self._dec_dev[i, :3 * B]
+        d.copy_(pin[:3 * B], non_blocking=True)
+        self._dec_ev[i].record()
+        self._dec_used[i] = True
+        max_seq = int(pos.max()) + 1
         o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
-        need = api.rx_decode_workspace_bytes(self.cfg, B, int(pos.max()) + 1)
+        need = api.rx_decode_workspace_bytes(self.cfg, B, max_seq)
         if need > self._ws.numel():            # split count depends on (B, max_seq): grow on demand
             self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
-        api.rx_decode(self.cfg, self._rtt, d32[2], d32[1], int(pos.max()) + 1, q, self.k_pool, self.v_pool, o,
-                      self._ws)
+        ev0 = self._tbeg()
+        api.rx_decode_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, q, k, v, d[:B], self.k_pool,
+                             self.v_pool, o, self._ws)
         nl = api.rx_last_launch_count()
-        self.stats["launches"] += launches + nl
+        self.stats["launches"] += nl
         if ev0 is not None:
-            # algorithmic bytes: unique pool rows read (K+V) + q + o + slot indices;
-            # every running request owns its rows here unless they share a cached prefix node,
-            # so count distinct slots
+            # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot indices,
+            # computed after the timed region from (slots, running, pos)
             self._tend(ev0, "decode", (self._slots_host, running.copy(), pos.copy()), nl)
         if self.gather is not None:
             o = self.gather(o)

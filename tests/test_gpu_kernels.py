@@ -276,3 +276,43 @@ def test_extend_many_items_ragged(h_q, h_kv, hd):
     ref = A.extend(pool, [rtt[b] for b in range(B)], pre, ext, q.float().numpy(), kn.float().numpy(),
                    vn.float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
     _cmp(o, ref, f"extend-many {h_q}/{h_kv}/{hd}")
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,lens", [(32, 8, 128, [1, 40, 700, 3000]), (8, 2, 64, [2, 300]),
+                                              (64, 8, 128, [8300, 5])])
+def test_decode_append_equals_store_then_decode(h_q, h_kv, hd, lens):
+    """rx_decode_append == rx_store_kv + rtt append + rx_decode, bit for bit (pool, table, output)."""
+    rng = np.random.default_rng(sum(lens))
+    B = len(lens)
+    S = sum(lens) + 64
+    kp = _vals(rng, S, h_kv, KIND_K, hd).cuda()
+    vp = _vals(rng, S, h_kv, KIND_V, hd).cuda()
+    stride = max(lens) + 4
+    perm = rng.permutation(np.arange(1, S))
+    rtt = np.zeros((B, stride), dtype=np.int32)
+    new = np.zeros(B, dtype=np.int32)
+    off = 0
+    for b, L in enumerate(lens):
+        rtt[b, :L - 1] = perm[off:off + L - 1]
+        new[b] = perm[off + L - 1]
+        off += L
+    q = _vals(rng, B, h_q, KIND_Q, hd).cuda()
+    kn = _vals(rng, B, h_kv, KIND_K, hd).cuda()
+    vn = _vals(rng, B, h_kv, KIND_V, hd).cuda()
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    seq = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, max(lens)) + 1, dtype=torch.uint8, device="cuda")
+    new_d = torch.from_numpy(new).cuda()
+    # path 1: store + decode
+    kp1, vp1, rtt1 = kp.clone(), vp.clone(), torch.from_numpy(rtt).cuda()
+    idx = torch.tensor([b * stride + L - 1 for b, L in enumerate(lens)], dtype=torch.int64, device="cuda")
+    rx.rx_store_kv(cfg, new_d, kn, vn, kp1, vp1, rtt1, idx)
+    o1 = torch.empty((B, h_q, hd), dtype=torch.bfloat16, device="cuda")
+    rx.rx_decode(cfg, rtt1, None, seq, max(lens), q, kp1, vp1, o1, ws)
+    # path 2: fused
+    kp2, vp2, rtt2 = kp.clone(), vp.clone(), torch.from_numpy(rtt).cuda()
+    o2 = torch.empty_like(o1)
+    rx.rx_decode_append(cfg, rtt2, None, seq, max(lens), q, kn, vn, new_d, kp2, vp2, o2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(kp1, kp2) and torch.equal(vp1, vp2) and torch.equal(rtt1, rtt2)
+    assert torch.equal(o1, o2)
