@@ -64,7 +64,8 @@ class _Req:
                 t = next_token(h, vocab)
                 toks.append(t)
                 hs.append(splitmix64_int((h ^ t) & MASK64))
-            full = (toks, hs)
+            # arrays, so every C-ABI call passes a pointer without conversion
+            full = (np.asarray(toks, dtype=np.int32), np.asarray(hs, dtype=np.uint64))
         self.tokens, self.hashes = full
         self.node = 0
         self.prefix = 0
@@ -121,6 +122,7 @@ class Engine:
         self.bank = None
         self._full_cache = {}
         self.timer = None
+        self._pin_cache = {}
         if not plan_only:
             hd = wl.shape.head_dim
             self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
@@ -281,7 +283,7 @@ class Engine:
         # one pinned staging block: [prefix | ext | qo_indptr] then the rtt rows
         stride = slots.shape[1]
         hdr = 3 * (B + 1)
-        stage = torch.empty(hdr + B * stride, dtype=torch.int32, pin_memory=True)
+        stage = self._pinned("ext", hdr + B * stride)
         sn = stage.numpy()
         sn[0:B] = prefix
         sn[B + 1:2 * B + 1] = ext
@@ -289,16 +291,21 @@ class Engine:
         sn[2 * B + 3:3 * B + 3] = np.cumsum(ext)
         sn[hdr:] = slots.reshape(-1)
         dstage = stage.to(dev, non_blocking=True)
-        self._stage_keep = stage                  # keep the pinned block alive until the copy lands
+        self._pinned_done("ext")
         self._rtt = dstage[hdr:].view(B, stride)
         self._B = B
         ws_n = api.rx_decode_workspace_bytes(self.cfg, B, stride)
         self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
-        # decode-step staging: two pinned blocks [new_slots | seq_lens | rows] (host may run 2 steps ahead)
-        self._dec_pin = [torch.empty((3 * B,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        self._dec_dev = torch.empty((2, 3 * B), dtype=torch.int32, device=dev)
-        self._dec_ev = [torch.cuda.Event(), torch.cuda.Event()]
-        self._dec_used = [False, False]
+        # decode-step staging: a ring of RING pinned blocks [new_slots | seq_lens | rows]; the host never
+        # needs GPU results (tree ops + precomputed inputs), so it may run up to RING steps ahead
+        RING = 64
+        for i, used in enumerate(getattr(self, "_dec_used", [])):   # previous batch's copies out of the ring
+            if used:
+                self._dec_ev[i].synchronize()
+        self._dec_pin = self._pinned("dec", RING * 3 * B).view(RING, 3 * B)
+        self._dec_dev = torch.empty((RING, 3 * B), dtype=torch.int32, device=dev)
+        self._dec_ev = [torch.cuda.Event() for _ in range(RING)]
+        self._dec_used = [False] * RING
         self._dec_n = 0
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         ev0 = self._tbeg()
@@ -326,10 +333,10 @@ class Engine:
         dev = self.device
         q, k, v = self.bank.dec[self._dec_i]
         self._dec_i += 1
-        i = self._dec_n & 1
+        i = self._dec_n % len(self._dec_ev)
         self._dec_n += 1
         if self._dec_used[i]:
-            self._dec_ev[i].synchronize()           # the H2D copy from two steps ago consumed this block
+            self._dec_ev[i].synchronize()           # the H2D copy from RING steps ago consumed this block
         pin = self._dec_pin[i]
         pn = pin.numpy()
         pn[0:B] = new_slots
@@ -357,6 +364,23 @@ class Engine:
             o = self.gather(o)
         if self.keep_outputs:
             self.outputs.append(("decode", o, {"B": B}))
+
+    # ------------------------------------------------------------------ pinned staging
+    def _pinned(self, name, n):
+        """Grow-only pinned int32 staging buffer; waits for its previous H2D copy before reuse."""
+        buf, ev = self._pin_cache.get(name, (None, None))
+        if ev is not None:
+            ev.synchronize()
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(n, 1024), dtype=torch.int32, pin_memory=True)
+        self._pin_cache[name] = (buf, None)
+        return buf[:n]
+
+    def _pinned_done(self, name):
+        buf, _ = self._pin_cache[name]
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pin_cache[name] = (buf, ev)
 
     # ------------------------------------------------------------------ timing hooks
     def enable_timing(self, on=True):
