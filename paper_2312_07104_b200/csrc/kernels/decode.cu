@@ -33,7 +33,7 @@ namespace rx {
 constexpr int kDecWarps = 4;
 constexpr int kBlk = 16;
 
-template <int HD, int STAGES_ = (HD == 128 ? 3 : 6)>
+template <int HD, int STAGES_ = (HD == 128 ? 2 : 6)>
 struct DecCfg {
   static constexpr int RB = HD * 2;                   // bytes per row
   static constexpr int BLK_BYTES = kBlk * RB;         // one K (or V) block
@@ -292,14 +292,14 @@ static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_
   return cudaPeekAtLastError();
 }
 
-// Pipeline depth per warp: 3 (default: 96 KB smem, 2 CTAs/SM) or 4 (128 KB, 1 CTA/SM)
-// for head_dim 128.  RX_DECODE_STAGES overrides it (development A/B knob).
+// Pipeline depth per warp for head_dim 128: 2 (default: 64 KB smem, 3 CTAs/SM;
+// measured 6.38 TB/s in the C3 step vs 5.96 for 3 stages / 2 CTAs per SM).  RX_DECODE_STAGES overrides it (development A/B knob).
 static int decode_stages() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("RX_DECODE_STAGES");
-    v = e ? atoi(e) : 3;
-    if (v != 2 && v != 3 && v != 4) v = 3;
+    v = e ? atoi(e) : 2;
+    if (v != 2 && v != 3 && v != 4) v = 2;
   }
   return v;
 }
@@ -310,9 +310,9 @@ cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch,
 #define RX_DEC_CASE(HD_, G_)                                                                  \
   if (head_dim == HD_ && G == G_) {                                                           \
     if (HD_ == 64) return launch_decode_t<HD_, G_, 6>(p, batch, st, launches);                \
-    if (stg == 2) return launch_decode_t<HD_, G_, 2>(p, batch, st, launches);                 \
     if (stg == 4) return launch_decode_t<HD_, G_, 4>(p, batch, st, launches);                 \
-    return launch_decode_t<HD_, G_, 3>(p, batch, st, launches);                               \
+    if (stg == 3) return launch_decode_t<HD_, G_, 3>(p, batch, st, launches);                 \
+    return launch_decode_t<HD_, G_, 2>(p, batch, st, launches);                               \
   }
   RX_DEC_CASE(64, 1) RX_DEC_CASE(64, 2) RX_DEC_CASE(64, 4) RX_DEC_CASE(64, 8)
   RX_DEC_CASE(128, 1) RX_DEC_CASE(128, 2) RX_DEC_CASE(128, 4) RX_DEC_CASE(128, 8)

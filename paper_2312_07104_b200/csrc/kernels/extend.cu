@@ -16,7 +16,8 @@
 //    the 128 slots of the tile are consecutive (the smallest-first allocator
 //    makes that the common case), or by cp.async.bulk.tensor tile::gather4
 //    (4 pool rows per instruction, issued by all 32 lanes) otherwise; all into
-//    128B-swizzled smem, STAGES-deep ring with full/empty mbarriers;
+//    128B-swizzled smem; separate K (3-deep) and V (2-deep) rings with
+//    full/empty mbarriers;
 //  * warp 1 = single-thread UMMA issuer: S = Q K^T (bf16 -> fp32 TMEM,
 //    double-buffered) then O += P V with P read from TMEM (A operand in
 //    tensor memory), all 128x128 / 128xHD tiles, cta_group::1;
@@ -24,8 +25,8 @@
 //    causal/length mask, online softmax in the log2 domain with lazy O
 //    rescaling (only when the running max grows by > 8), P packed to bf16 and
 //    tcgen05.st over the S columns; epilogue O / l -> bf16 -> global;
-//  * warps 2-3: TMEM allocation and the fused store of this tile's new K/V
-//    rows into their slots.
+//  * warp 2: TMEM allocation and the fused store of this tile's new K/V rows
+//    into their slots; warp 3: V producer (K and V rings are separate).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -57,16 +58,19 @@ struct ExtCfg {
   static constexpr int NCB = HD / 64;                         // 64-column blocks
   static constexpr int Q_BYTES = NCB * 128 * kTileRowBytes;   // one Q tile (double-buffered)
   static constexpr int KV_BYTES = NCB * kBN * kTileRowBytes;  // one K (or V) tile
-  static constexpr int STAGES = HD == 128 ? 2 : 3;
-  static constexpr int SMEM_DATA = 2 * Q_BYTES + STAGES * 2 * KV_BYTES;
+  // K and V live in separate rings: K_j is released as soon as S_j = Q K_j^T
+  // retires, V_j only after P_j V_j, so K can run further ahead (its load
+  // latency is on the critical path of the next softmax).
+  static constexpr int KS = HD == 128 ? 3 : 4;
+  static constexpr int VS = HD == 128 ? 2 : 3;
+  static constexpr int SMEM_DATA = 2 * Q_BYTES + (KS + VS) * KV_BYTES;
   static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 512;                  // S0 | S1 | O0 | O1
   static constexpr uint32_t O_COL = 256;                      // O buffer b at O_COL + b*HD
 };
 
-// One work item = (q tile t, kv head g, request b).  Items are enumerated
-// heaviest first (largest t first: causal work grows with t) and dealt to the
-// persistent CTAs round-robin; every role of a CTA walks the same list.
+// One work item = (q tile t, kv head g, request b), dealt to the persistent
+// CTAs round-robin; every role of a CTA walks the same list.
 struct ExtItem {
   int b, g, t, P, ext, qo, n_pre, n_tiles;
   const int32_t* slots;
@@ -74,11 +78,13 @@ struct ExtItem {
 
 template <int TOK>
 __device__ __forceinline__ bool ext_item(const ExtendParams& p, int qt, int w, ExtItem& it) {
-  const int per_t = p.h_kv * p.batch;
-  it.t = qt - 1 - w / per_t;
-  const int rem = w % per_t;
-  it.g = rem % p.h_kv;
-  it.b = rem / p.h_kv;
+  // (request, kv head) outer, q tile inner (heaviest first): the q tiles of
+  // one (b, g) run on neighbouring CTAs at the same time, so that head's
+  // cached prefix is read from HBM once and re-served from L2.
+  const int bg = w / qt;
+  it.t = qt - 1 - w % qt;
+  it.g = bg % p.h_kv;
+  it.b = bg / p.h_kv;
   it.ext = p.extend_lens[it.b];
   if (it.t * TOK >= it.ext) return false;
   it.P = p.prefix_lens[it.b];
@@ -99,13 +105,16 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sq = smem_u32(smem);                 // Q buffer qb at sq + qb*Q_BYTES
-  const uint32_t skv = sq + 2 * C::Q_BYTES;           // stage s: K at skv + s*2*KV, V at +KV
+  const uint32_t sk = sq + 2 * C::Q_BYTES;            // K stage s at sk + s*KV_BYTES
+  const uint32_t sv_ = sk + C::KS * C::KV_BYTES;      // V stage s at sv_ + s*KV_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA);
   uint64_t* q_full = bars;                            // [2]
   uint64_t* q_empty = bars + 2;                       // [2]
-  uint64_t* kv_full = bars + 4;                       // [STAGES]
-  uint64_t* kv_empty = kv_full + C::STAGES;           // [STAGES]
-  uint64_t* s_full = kv_empty + C::STAGES;            // [2]
+  uint64_t* k_full = bars + 4;                        // [KS]
+  uint64_t* k_empty = k_full + C::KS;                 // [KS]
+  uint64_t* v_full = k_empty + C::KS;                 // [VS]
+  uint64_t* v_empty = v_full + C::VS;                 // [VS]
+  uint64_t* s_full = v_empty + C::VS;                 // [2]
   uint64_t* p_full = s_full + 2;                      // [2]
   uint64_t* o_done = p_full + 2;                      // one phase per P.V
   uint64_t* o_ready = o_done + 1;                     // [2] one phase per item (its last P.V)
@@ -125,9 +134,13 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(o_ready + i, 1);
       mbar_init(o_free + i, 128);
     }
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(kv_full + s, 1);
-      mbar_init(kv_empty + s, 1);
+    for (int s = 0; s < C::KS; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < C::VS; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
     }
     mbar_init(o_done, 1);
     fence_barrier_init();
@@ -138,33 +151,43 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------------------ producers: warp 0 = Q + K, warp 3 = V
+    const bool is_v = warp == 3;
+    const int NS = is_v ? C::VS : C::KS;
+    uint64_t* full = is_v ? v_full : k_full;
+    uint64_t* empty = is_v ? v_empty : k_empty;
+    const uint32_t base_s = is_v ? sv_ : sk;
+    const CUtensorMap* m_pool = is_v ? &maps.vpool : &maps.kpool;
+    const CUtensorMap* m_gat = is_v ? &maps.vgat : &maps.kgat;
+    const CUtensorMap* m_new = is_v ? &maps.vnew : &maps.knew;
     if (lane == 0) {
-      tma_prefetch_desc(&maps.q);
-      tma_prefetch_desc(&maps.knew);
-      tma_prefetch_desc(&maps.kpool);
-      tma_prefetch_desc(&maps.kgat);
+      if (!is_v) tma_prefetch_desc(&maps.q);
+      tma_prefetch_desc(m_new);
+      tma_prefetch_desc(m_pool);
+      tma_prefetch_desc(m_gat);
     }
     const int oob_row = int(p.num_slots * p.h_kv);  // coordinate past the end: TMA zero-fills
     int it = 0, jg = 0;
     ExtItem I;
     for (int w = blockIdx.x; w < W; w += gridDim.x) {
       if (!ext_item<TOK>(p, qt, w, I)) continue;
-      const int qb = it & 1;
-      if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
-      if (lane == 0) {
-        mbar_arrive_expect_tx(q_full + qb, C::Q_BYTES);
+      if (!is_v) {
+        const int qb = it & 1;
+        if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(q_full + qb, C::Q_BYTES);
 #pragma unroll
-        for (int c = 0; c < C::NCB; ++c)
-          tma_load_3d(sq + qb * C::Q_BYTES + c * 128 * kTileRowBytes, &maps.q, q_full + qb, c * 64, I.g * G,
-                      I.qo + I.t * TOK);
+          for (int c = 0; c < C::NCB; ++c)
+            tma_load_3d(sq + qb * C::Q_BYTES + c * 128 * kTileRowBytes, &maps.q, q_full + qb, c * 64, I.g * G,
+                        I.qo + I.t * TOK);
+        }
       }
       for (int j = 0; j < I.n_tiles; ++j, ++jg) {
-        const int st = jg % C::STAGES, rnd = jg / C::STAGES;
-        mbar_wait(kv_empty + st, (rnd & 1) ^ 1);
-        const uint32_t kd = skv + st * 2 * C::KV_BYTES, vd = kd + C::KV_BYTES;
-        if (lane == 0) mbar_arrive_expect_tx(kv_full + st, 2 * C::KV_BYTES);
+        const int st = jg % NS, rnd = jg / NS;
+        mbar_wait(empty + st, (rnd & 1) ^ 1);
+        const uint32_t d = base_s + st * C::KV_BYTES;
+        if (lane == 0) mbar_arrive_expect_tx(full + st, C::KV_BYTES);
         __syncwarp();
         if (j < I.n_pre) {
           const int base = j * kBN + 4 * lane;
@@ -179,29 +202,23 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           if (contig) {
             if (lane == 0) {
 #pragma unroll
-              for (int c = 0; c < C::NCB; ++c) {
-                tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.kpool, kv_full + st, c * 64, I.g, s0);
-                tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vpool, kv_full + st, c * 64, I.g, s0);
-              }
+              for (int c = 0; c < C::NCB; ++c)
+                tma_load_3d(d + c * kBN * kTileRowBytes, m_pool, full + st, c * 64, I.g, s0);
             }
           } else {
             int r[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) r[i] = sl[i] > 0 ? sl[i] * p.h_kv + I.g : oob_row;
 #pragma unroll
-            for (int c = 0; c < C::NCB; ++c) {
-              const uint32_t off = c * kBN * kTileRowBytes + 4 * lane * kTileRowBytes;
-              tma_gather4(kd + off, &maps.kgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
-              tma_gather4(vd + off, &maps.vgat, kv_full + st, c * 64, r[0], r[1], r[2], r[3]);
-            }
+            for (int c = 0; c < C::NCB; ++c)
+              tma_gather4(d + c * kBN * kTileRowBytes + 4 * lane * kTileRowBytes, m_gat, full + st, c * 64, r[0],
+                          r[1], r[2], r[3]);
           }
         } else if (lane == 0) {
           const int nn = j - I.n_pre;
 #pragma unroll
-          for (int c = 0; c < C::NCB; ++c) {
-            tma_load_3d(kd + c * kBN * kTileRowBytes, &maps.knew, kv_full + st, c * 64, I.g, I.qo + nn * kBN);
-            tma_load_3d(vd + c * kBN * kTileRowBytes, &maps.vnew, kv_full + st, c * 64, I.g, I.qo + nn * kBN);
-          }
+          for (int c = 0; c < C::NCB; ++c)
+            tma_load_3d(d + c * kBN * kTileRowBytes, m_new, full + st, c * 64, I.g, I.qo + nn * kBN);
         }
       }
       ++it;
@@ -222,10 +239,10 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         if (it >= 2) mbar_wait(o_free + qb, ((it >> 1) - 1) & 1);  // epilogue of item it-2 read O[qb]
         auto issue_s = [&](int j) {
           const int g_ = jg + j;
-          const int st = g_ % C::STAGES;
-          mbar_wait(kv_full + st, (g_ / C::STAGES) & 1);
+          const int st = g_ % C::KS;
+          mbar_wait(k_full + st, (g_ / C::KS) & 1);
           tc_fence_after();
-          const uint32_t kb = skv + st * 2 * C::KV_BYTES;
+          const uint32_t kb = sk + st * C::KV_BYTES;
           const uint32_t t_s = tmem + (g_ & 1) * 128;
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
@@ -234,6 +251,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
                     umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
           }
           tc_commit(s_full + (g_ & 1));
+          tc_commit(k_empty + st);                          // K_g is free once S_g retires
           if (j == I.n_tiles - 1) tc_commit(q_empty + qb);  // last read of this Q buffer issued
         };
         issue_s(0);
@@ -242,14 +260,15 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           const int g_ = jg + j;
           mbar_wait(p_full + (g_ & 1), (g_ >> 1) & 1);
           tc_fence_after();
-          const int st = g_ % C::STAGES;
-          const uint32_t vb = skv + st * 2 * C::KV_BYTES + C::KV_BYTES;
+          const int st = g_ % C::VS;
+          mbar_wait(v_full + st, (g_ / C::VS) & 1);
+          const uint32_t vb = sv_ + st * C::KV_BYTES;
           const uint32_t t_p = tmem + (g_ & 1) * 128;
 #pragma unroll
           for (int k = 0; k < kBN / 16; ++k)
             umma_ts(t_o, t_p + k * 8, umma_desc_sw128(vb + k * 2048, kBN * kTileRowBytes, 1024), idesc_o,
                     (j > 0 || k > 0) ? 1u : 0u);
-          tc_commit(kv_empty + st);
+          tc_commit(v_empty + st);
           tc_commit(o_done);
         }
         tc_commit(o_ready + qb);
@@ -278,14 +297,22 @@ __global__ void __launch_bounds__(kExtThreads, 1)
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c) tmem_ld32(t_s + c * 32, sv + c * 32);
         tmem_ld_wait();
-        // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel
+        // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel.
+        // Scores stay raw (unscaled); the scale is folded into the exp2 FFMA.
         const int lim = j < I.n_pre ? I.P - j * kBN - 1 : rel - (j - I.n_pre) * kBN;
+        const bool full = __all_sync(0xffffffffu, lim >= kBN - 1);   // warp-uniform
         float mx = -INFINITY;
+        if (full) {
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) {
-          sv[c] = c <= lim ? sv[c] * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, sv[c]);
+          for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, sv[c]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < kBN; ++c) {
+            sv[c] = c <= lim ? sv[c] : -INFINITY;
+            mx = fmaxf(mx, sv[c]);
+          }
         }
+        mx *= p.scale_log2;
         // Lazy rescale, decided per WARP: tcgen05.ld/st are .sync.aligned
         // warp-collective, so the O round trip must not diverge across rows.
         // Lanes whose max did not grow get corr = 1.
@@ -315,11 +342,25 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         }
         uint32_t pk[kBN / 2];
         float rs = 0.f;
+        const float sc = p.scale_log2, nm = -m_ref;
+        if (full) {
+          // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
+          // every 4th column is evaluated on the FMA pipe instead.
 #pragma unroll
-        for (int c = 0; c < kBN / 2; ++c) {
-          const float e0 = fast_exp2(sv[2 * c] - m_ref), e1 = fast_exp2(sv[2 * c + 1] - m_ref);
-          rs += e0 + e1;
-          pk[c] = pack_bf16(e0, e1);
+          for (int c = 0; c < kBN / 2; ++c) {
+            const float x0 = fmaf(sv[2 * c], sc, nm), x1 = fmaf(sv[2 * c + 1], sc, nm);
+            const float e0 = fast_exp2(x0);
+            const float e1 = (c & 1) ? exp2_poly3(x1) : fast_exp2(x1);
+            rs += e0 + e1;
+            pk[c] = pack_bf16(e0, e1);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < kBN / 2; ++c) {
+            const float e0 = fast_exp2(fmaf(sv[2 * c], sc, nm)), e1 = fast_exp2(fmaf(sv[2 * c + 1], sc, nm));
+            rs += e0 + e1;
+            pk[c] = pack_bf16(e0, e1);
+          }
         }
         l += rs;
         tmem_st32(t_s, pk);
@@ -358,14 +399,14 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       ++it;
     }
   } else {
-    // ------------------------------------------------------------ warps 2-3: fused KV store (A5)
-    const int tid = threadIdx.x - 64;              // 0..63
+    // ------------------------------------------------------------ warp 2: fused KV store (A5)
+    const int tid = lane;
     constexpr int VPR = HD / 8;                     // 16-byte vectors per head row
     ExtItem I;
     for (int w = blockIdx.x; w < W; w += gridDim.x) {
       if (!ext_item<TOK>(p, qt, w, I)) continue;
       const int n_tok = min(I.ext, (I.t + 1) * TOK) - I.t * TOK;
-      for (int idx = tid; idx < n_tok * VPR; idx += 64) {
+      for (int idx = tid; idx < n_tok * VPR; idx += 32) {
         const int i = idx / VPR, c = idx % VPR;
         const int relp = I.t * TOK + i;
         const int64_t slot = I.slots[I.P + relp];

@@ -1,0 +1,51 @@
+"""Fake tensor parallelism on one GPU: the P head shards of a
+TP run, executed one after another on the same device, with exactly the
+local shapes a P-GPU run uses.
+
+* every shard's radix-tree trace is identical ("the tree
+  operations are the same") and equals the 1-GPU trace;
+* the shards' outputs, reassembled in global head order, match the 1-GPU run
+  within the attention tolerance (different local shapes may change the
+  split-KV partition, hence summation order, so not bitwise).
+"""
+import numpy as np
+import pytest
+import torch
+
+from rxgen import workloads
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2312_07104_b200.engine import Engine, plan_and_bank
+
+
+def _run(wl, rank=0, size=1):
+    _, bank = plan_and_bank(wl, "cuda", tp_rank=rank, tp_size=size)
+    e = Engine(wl, "cuda", tp_rank=rank, tp_size=size, record=True, keep_outputs=True)
+    e.run_workload(bank)
+    torch.cuda.synchronize()
+    return e
+
+
+@pytest.mark.parametrize("make,P", [
+    (lambda: workloads.c5(n_req=6, prefix=600, question=40, decode=5, num_slots=8192), 2),
+    (lambda: workloads.c5(n_req=6, prefix=600, question=40, decode=5, num_slots=8192), 8),
+    (lambda: workloads.c3(sessions=4, turns=2, in_lo=30, in_hi=90, out_lo=4, out_hi=9, num_slots=8192), 8),
+    (lambda: workloads.c1(), 4),
+])
+def test_fake_tp_matches_single_gpu(make, P):
+    wl = make()
+    full = _run(wl)
+    shards = [_run(wl, r, P) for r in range(P)]
+    for s in shards:
+        assert s.trace == full.trace
+    worst = 0.0
+    for ci, (kind, o_full, _) in enumerate(full.outputs):
+        parts = [s.outputs[ci][1] for s in shards]
+        assert all(s.outputs[ci][0] == kind for s in shards)
+        o_tp = torch.cat(parts, dim=1)                     # rank-major = global head order
+        assert o_tp.shape == o_full.shape
+        err = (o_tp.float() - o_full.float()).abs().max().item()
+        worst = max(worst, err)
+    assert worst <= 2e-2, worst
