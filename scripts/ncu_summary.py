@@ -1,0 +1,54 @@
+"""Summarise an `ncu --set full` report into a few lines for profiles/.
+
+    python scripts/ncu_summary.py gpurun_out/full_C3_decode.ncu-rep > profiles/r1_ncu_decode_summary.txt
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_bytes.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__block_size",
+    "launch__shared_mem_per_block_dynamic",
+    "launch__occupancy_limit_shared_mem",
+    "smsp__average_warp_latency_issue_stalled_long_scoreboard",
+]
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    print(f"# {path}")
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+        print(f"kernel: {name}")
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                print(f"  {k} = {r[i]} {units[i]}")
+        # top stall reasons
+        stalls = [(hdr[i], r[i]) for i in range(len(hdr))
+                  if hdr[i].startswith("smsp__average_warp_latency_issue_stalled_") and hdr[i].endswith("_per_warp_active.pct")]
+        stalls = sorted(((h, float(v)) for h, v in stalls if v.replace('.', '', 1).isdigit()), key=lambda x: -x[1])[:6]
+        for h, v in stalls:
+            print(f"  stall {h.replace('smsp__average_warp_latency_issue_stalled_', '')} = {v:.1f}")
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        main(p)
