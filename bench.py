@@ -261,8 +261,6 @@ def main():
         hbank.ext = [tuple(t.cpu().pin_memory() for t in tr) for tr in bank.ext]
         hbank.dec = [tuple(t.cpu().pin_memory() for t in tr) for tr in bank.dec]
         h2d = sum(t.numel() * t.element_size() for lst in (hbank.ext, hbank.dec) for tr in lst for t in tr)
-        outs_host = []
-        d2h = [0]
 
         class DevBank:
             """Moves each call's inputs host->device right before the call (inside the timed region)."""
@@ -278,7 +276,23 @@ def main():
                 return tuple(t.to(dev, non_blocking=True) for t in self.lst[i])
 
         eng.enable_timing(False)
-        eng.keep_outputs = True
+        # every call's output lands in a preallocated pinned host buffer (D2H right after the call,
+        # overlapping the following work); sizes come from the plan
+        out_host = []
+        for c in plan.calls:
+            rows = len(c.hashes)
+            hq = eng.hq * world
+            out_host.append(torch.empty((rows, hq, wl.shape.head_dim), dtype=torch.bfloat16, pin_memory=True))
+        d2h = [sum(t.numel() * t.element_size() for t in out_host)]
+        slot = [0]
+
+        def sink(kind, o):
+            dst = out_host[slot[0]]
+            dst.view(o.shape).copy_(o, non_blocking=True) if o.is_contiguous() else dst.copy_(o.reshape(dst.shape),
+                                                                                               non_blocking=True)
+            slot[0] += 1
+
+        eng.sink = sink
         e2e_times = []
         for it in range(max(1, args.steps)):
             flush.fill_(1)
@@ -286,15 +300,14 @@ def main():
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
+            slot[0] = 0
             a.record()
             eng.reset()
             eng.run_workload(DevBank(hbank))
-            outs = [o.to("cpu", non_blocking=True) for _, o, _ in eng.outputs]
             b.record()
             torch.cuda.synchronize()
             e2e_times.append(a.elapsed_time(b))
-            d2h[0] = sum(o.numel() * o.element_size() for o in outs)
-            eng.outputs = []
+        eng.sink = None
         e_ms = sum(e2e_times)
         if world > 1:
             tt = torch.tensor([e_ms], device=dev)

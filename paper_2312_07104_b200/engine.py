@@ -123,6 +123,7 @@ class Engine:
         self._full_cache = {}
         self.timer = None
         self._pin_cache = {}
+        self.sink = None                     # callable(kind, o) invoked after every attention call
         if not plan_only:
             hd = wl.shape.head_dim
             self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
@@ -320,6 +321,8 @@ class Engine:
             self._tend(ev0, "extend", flops, nl)
         if self.gather is not None:
             o = self.gather(o)
+        if self.sink is not None:
+            self.sink("extend", o)
         if self.keep_outputs:
             self.outputs.append(("extend", o, {"ext": ext.tolist()}))
 
@@ -362,6 +365,8 @@ class Engine:
             self._tend(ev0, "decode", (self._slots_host, running.copy(), pos.copy()), nl)
         if self.gather is not None:
             o = self.gather(o)
+        if self.sink is not None:
+            self.sink("decode", o)
         if self.keep_outputs:
             self.outputs.append(("decode", o, {"B": B}))
 
