@@ -136,6 +136,26 @@ rx_status rx_free(rx_cache* c, const int32_t* slots, int64_t n);
 rx_status rx_alloc_evict(rx_cache* c, int64_t n, int32_t* out, int64_t* evicted,
                          rx_evict_cb cb, void* user);
 
+/* Batched forms for a whole scheduling step (one C call instead of one per
+ * request; same semantics as calling the single-request function for
+ * b = 0 .. batch-1 in order, including the clock ticks).  Request b's tokens
+ * are tokens[offsets[b] .. offsets[b+1]) (offsets: int64 [batch+1]).
+ *   rx_match_prefix_batch: nodes[b], matched[b]; slots_out (may be null) uses
+ *     the same layout as tokens and receives each request's matched slots.
+ *   rx_inc_ref_batch: deltas[b] (may be null) = Δevictable of request b.
+ *   rx_finish_batch: Alg. 1 "process finished requests":
+ *     rx_dec_ref(nodes[b]) then rx_insert(tokens_b, slots_b) for each b;
+ *     slots has the same layout as tokens; d_evict[b], new_cached[b],
+ *     dup_freed[b] may be null.
+ * On an error the call stops at the failing request and returns its status;
+ * requests before it have been processed. */
+rx_status rx_match_prefix_batch(rx_cache* c, int32_t batch, const int32_t* tokens, const int64_t* offsets,
+                                rx_node* nodes, int64_t* matched, int32_t* slots_out);
+rx_status rx_inc_ref_batch(rx_cache* c, int32_t batch, const rx_node* nodes, int64_t* deltas);
+rx_status rx_finish_batch(rx_cache* c, int32_t batch, const rx_node* nodes, const int32_t* tokens,
+                          const int64_t* offsets, const int32_t* slots, int64_t* d_evict,
+                          int64_t* new_cached, int64_t* dup_freed);
+
 /* Pure queries (Alg. 1 "T.evictable_size() + P.available_size()", P:534;
  * SPEC S:149-156).  evictable = tokens on non-root nodes with ref 0 (pins
  * propagate to the root, so these are exactly the peelable nodes). */

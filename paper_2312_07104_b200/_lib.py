@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "librx.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2312_07104_b200.build` "
+    raise ImportError(f"{LIB_PATH} not built: run `python paper_2312_07104_b200/build.py` "
                       "(or __graft_entry__.build()); there is no CPU fallback")
 
 lib = C.CDLL(LIB_PATH)
@@ -42,6 +42,9 @@ SIGNATURES = {
     "rx_alloc": (C.c_int, [vp, i64, P32]),
     "rx_free": (C.c_int, [vp, P32, i64]),
     "rx_alloc_evict": (C.c_int, [vp, i64, P32, P64, EVICT_CB, vp]),
+    "rx_match_prefix_batch": (C.c_int, [vp, i32, P32, P64, P64, P64, P32]),
+    "rx_inc_ref_batch": (C.c_int, [vp, i32, P64, P64]),
+    "rx_finish_batch": (C.c_int, [vp, i32, P64, P32, P64, P32, P64, P64, P64]),
     "rx_evictable_size": (i64, [vp]),
     "rx_total_cached": (i64, [vp]),
     "rx_available": (i64, [vp]),

@@ -116,6 +116,38 @@ class RadixCache:
         s = _i32(slots)
         _check(lib.rx_free(self._h, _p32(s), len(s)), "rx_free")
 
+    # -------------------------------------------------------------- batched (one C call per step)
+    def rx_match_prefix_batch(self, tokens_concat, offsets):
+        """-> (nodes int64[B], matched int64[B], slots int32 (same layout as tokens_concat))"""
+        t = _i32(tokens_concat)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        B = len(off) - 1
+        nodes = np.empty(B, dtype=np.int64)
+        matched = np.empty(B, dtype=np.int64)
+        slots = np.empty(max(len(t), 1), dtype=_I32)
+        _check(lib.rx_match_prefix_batch(self._h, B, _p32(t), off.ctypes.data_as(P64), nodes.ctypes.data_as(P64),
+                                         matched.ctypes.data_as(P64), _p32(slots)), "rx_match_prefix_batch")
+        return nodes, matched, slots
+
+    def rx_inc_ref_batch(self, nodes):
+        n = np.ascontiguousarray(nodes, dtype=np.int64)
+        d = np.empty(len(n), dtype=np.int64)
+        _check(lib.rx_inc_ref_batch(self._h, len(n), n.ctypes.data_as(P64), d.ctypes.data_as(P64)),
+               "rx_inc_ref_batch")
+        return d
+
+    def rx_finish_batch(self, nodes, tokens_concat, offsets, slots_concat):
+        """dec_ref + insert per request -> (d_evict, new_cached, dup_freed), each int64[B]"""
+        n = np.ascontiguousarray(nodes, dtype=np.int64)
+        t, s = _i32(tokens_concat), _i32(slots_concat)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        B = len(n)
+        d, nc, nd = (np.empty(B, dtype=np.int64) for _ in range(3))
+        _check(lib.rx_finish_batch(self._h, B, n.ctypes.data_as(P64), _p32(t), off.ctypes.data_as(P64), _p32(s),
+                                   d.ctypes.data_as(P64), nc.ctypes.data_as(P64), nd.ctypes.data_as(P64)),
+               "rx_finish_batch")
+        return d, nc, nd
+
     def rx_evictable_size(self) -> int:
         return lib.rx_evictable_size(self._h)
 

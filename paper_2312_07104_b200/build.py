@@ -1,8 +1,8 @@
 """Build librx.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2312_07104_b200.build            # build if stale
-    python -m paper_2312_07104_b200.build --force    # rebuild everything
-    python -m paper_2312_07104_b200.build --ptxas-v  # print register / smem usage
+    python paper_2312_07104_b200/build.py          # build if stale
+    python paper_2312_07104_b200/build.py --force # rebuild everything
+    python paper_2312_07104_b200/build.py --ptxas-v # print register / smem usage
 
 Sources: csrc/host/*.cc (radix tree, pure host C++17) and csrc/kernels/*.cu
 (sm_100a kernels + C-ABI wrappers).  Objects go to build/ next to this file.

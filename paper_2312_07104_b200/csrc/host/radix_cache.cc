@@ -364,6 +364,46 @@ rx_status rx_alloc_evict(rx_cache* c, int64_t n, int32_t* out, int64_t* evicted,
   return rx_alloc(c, n, out);
 }
 
+rx_status rx_match_prefix_batch(rx_cache* c, int32_t batch, const int32_t* tokens, const int64_t* offsets,
+                                rx_node* nodes, int64_t* matched, int32_t* slots_out) {
+  if (!c || batch < 0 || (batch > 0 && (!tokens || !offsets || !nodes || !matched))) return RX_E_INVALID;
+  for (int32_t b = 0; b < batch; ++b) {
+    const int64_t o = offsets[b], n = offsets[b + 1] - o;
+    rx_status st = rx_match_prefix(c, tokens + o, n, nodes + b, matched + b, slots_out ? slots_out + o : nullptr);
+    if (st != RX_OK) return st;
+  }
+  return RX_OK;
+}
+
+rx_status rx_inc_ref_batch(rx_cache* c, int32_t batch, const rx_node* nodes, int64_t* deltas) {
+  if (!c || batch < 0 || (batch > 0 && !nodes)) return RX_E_INVALID;
+  for (int32_t b = 0; b < batch; ++b) {
+    int64_t d = 0;
+    rx_status st = rx_inc_ref(c, nodes[b], &d);
+    if (st != RX_OK) return st;
+    if (deltas) deltas[b] = d;
+  }
+  return RX_OK;
+}
+
+rx_status rx_finish_batch(rx_cache* c, int32_t batch, const rx_node* nodes, const int32_t* tokens,
+                          const int64_t* offsets, const int32_t* slots, int64_t* d_evict, int64_t* new_cached,
+                          int64_t* dup_freed) {
+  if (!c || batch < 0 || (batch > 0 && (!nodes || !tokens || !offsets || !slots))) return RX_E_INVALID;
+  for (int32_t b = 0; b < batch; ++b) {
+    int64_t d = 0, nc = 0, nd = 0;
+    rx_status st = rx_dec_ref(c, nodes[b], &d);
+    if (st != RX_OK) return st;
+    const int64_t o = offsets[b];
+    st = rx_insert(c, tokens + o, slots + o, offsets[b + 1] - o, &nc, &nd);
+    if (st != RX_OK) return st;
+    if (d_evict) d_evict[b] = d;
+    if (new_cached) new_cached[b] = nc;
+    if (dup_freed) dup_freed[b] = nd;
+  }
+  return RX_OK;
+}
+
 int64_t rx_evictable_size(const rx_cache* c) { return c ? c->evictable : -1; }
 int64_t rx_total_cached(const rx_cache* c) { return c ? c->cached : -1; }
 int64_t rx_available(const rx_cache* c) { return c ? c->free_slots.count() : -1; }

@@ -162,23 +162,30 @@ class Engine:
     def _match(self, rs):
         """match_prefix for every request (Alg. 1); usable prefix capped at n-1 (R11)."""
         c = self.cache
-        for r in rs:
-            node, m, sl = c.rx_match_prefix(r.tokens[:r.n_prompt])
+        if not rs:
+            return
+        toks = np.concatenate([r.tokens[:r.n_prompt] for r in rs])
+        off = np.zeros(len(rs) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([r.n_prompt for r in rs])
+        nodes, matched, sl = c.rx_match_prefix_batch(toks, off)        # one C call per step
+        for b, r in enumerate(rs):
+            m = int(matched[b])
+            s = sl[off[b]:off[b] + m]
             if self.record:
-                self._rec("match", r.rid, m, tuple(int(x) for x in sl))
-            r.node = node
+                self._rec("match", r.rid, m, tuple(int(x) for x in s))
+            r.node = int(nodes[b])
             r.matched = m
             r.prefix = min(m, r.n_prompt - 1)
-            r.slots = sl[:r.prefix]
+            r.slots = s[:r.prefix]
 
     def run_batch(self, reqs):
         """One batch admitted whole: match, pin every request, run to completion."""
         t0 = time.perf_counter()
         rs = self._reqs(reqs)
         self._match(rs)
-        for r in rs:
-            d = self.cache.rx_inc_ref(r.node)
-            self._rec("inc_ref", r.rid, d)
+        deltas = self.cache.rx_inc_ref_batch([r.node for r in rs])
+        for r, d in zip(rs, deltas):
+            self._rec("inc_ref", r.rid, int(d))
         self.stats["tree_s"] += time.perf_counter() - t0
         return self._run_matched(rs)
 
@@ -240,9 +247,7 @@ class Engine:
         self._slots_host = slots
         self._extend(rs, slots, prefix, ext)
         t0 = time.perf_counter()
-        for b, r in enumerate(rs):
-            if r.n_out == 0:
-                self._finish(r, slots[b])
+        self._finish_many(rs, np.nonzero(n_out == 0)[0], slots)
         running = np.nonzero(n_out > 0)[0]
         self.stats["tree_s"] += time.perf_counter() - t0
         step = 0
@@ -256,18 +261,28 @@ class Engine:
             step += 1
             t0 = time.perf_counter()
             done = n_out[running] <= step
-            for b in running[done]:
-                self._finish(rs[b], slots[b])
+            if done.any():
+                self._finish_many(rs, running[done], slots)
             running = running[~done]
             self.stats["tree_s"] += time.perf_counter() - t0
         self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
         return rs
 
-    def _finish(self, r: _Req, row_slots):
-        c = self.cache
-        self._rec("dec_ref", r.rid, c.rx_dec_ref(r.node))
-        n = r.n_prompt + r.n_out
-        self._rec("insert", r.rid, *c.rx_insert(r.tokens[:n], row_slots[:n]))
+    def _finish_many(self, rs, idx, slots):
+        """Alg. 1 finished requests: dec_ref then insert(prompt + outputs), in batch order,
+        one C call for all of them."""
+        if len(idx) == 0:
+            return
+        lens = np.array([rs[b].n_prompt + rs[b].n_out for b in idx], dtype=np.int64)
+        off = np.zeros(len(idx) + 1, dtype=np.int64)
+        off[1:] = np.cumsum(lens)
+        toks = np.concatenate([rs[b].tokens[:n] for b, n in zip(idx, lens)])
+        sl = np.concatenate([slots[b, :n] for b, n in zip(idx, lens)])
+        d, nc, nd = self.cache.rx_finish_batch([rs[b].node for b in idx], toks, off, sl)
+        if self.record:
+            for i, b in enumerate(idx):
+                self._rec("dec_ref", rs[b].rid, int(d[i]))
+                self._rec("insert", rs[b].rid, int(nc[i]), int(nd[i]))
 
     # ------------------------------------------------------------------ attention calls
     def _extend(self, rs, slots, prefix, ext):
