@@ -165,10 +165,16 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
   p.h_kv = cfg->h_kv;
   p.num_slots = num_slots;
   p.scale_log2 = cfg->sm_scale * 1.4426950408889634f;
-  cudaError_t e = rx::launch_extend(cfg->head_dim, cfg->h_q / cfg->h_kv, p, d_q, total_new, batch, max_extend_len,
-                                    static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // A5: new K/V rows into their slots (independent of the attention reads:
+  // new slots are never prefix slots, and the attention reads k_new/v_new)
+  cudaError_t e = rx::launch_extend_store(total_new, batch, cfg->h_kv * cfg->head_dim * 2, d_qo_indptr, d_extend_lens,
+                                          d_prefix_lens, d_rows, d_rtt, rtt_stride, d_k_new, d_v_new, d_k_pool,
+                                          d_v_pool, st);
   if (e != cudaSuccess) return RX_E_CUDA;
-  g_last_launches = 1;
+  e = rx::launch_extend(cfg->head_dim, cfg->h_q / cfg->h_kv, p, d_q, total_new, batch, max_extend_len, st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  g_last_launches = 2;
   return RX_OK;
 }
 

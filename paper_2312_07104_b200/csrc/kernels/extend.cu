@@ -5,8 +5,8 @@
 //     o = softmax_{i <= p}(scale * q . K[i]) V[i]
 // where K/V rows 0..prefix_len-1 are the CACHED prefix, read from the pool
 // through rtt ("reduces the computation of prefill"), and
-// rows prefix_len.. are this call's k_new/v_new — which the same launch also
-// stores into their pool slots (A5 fused into A6).
+// rows prefix_len.. are this call's k_new/v_new (read directly; rx_extend
+// stores them into their pool slots with a separate launch, A5).
 //
 // B200 design (one CTA per (q tile, kv head, request)):
 //  * M = 128 rows per tile = (128/G tokens) x (G heads of one kv group): GQA
@@ -25,8 +25,10 @@
 //    causal/length mask, online softmax in the log2 domain with lazy O
 //    rescaling (only when the running max grows by > 8), P packed to bf16 and
 //    tcgen05.st over the S columns; epilogue O / l -> bf16 -> global;
-//  * warp 2: TMEM allocation and the fused store of this tile's new K/V rows
-//    into their slots; warp 3: V producer (K and V rings are separate).
+//  * warp 2: TMEM allocation; warp 3: V producer (K and V rings are separate).
+//  * A5 (store new K/V into their slots) runs as a separate, fully parallel
+//    kernel just before on the same stream (store.cu): inside this kernel it
+//    was a latency-bound serial copy on one warp that outlived short items.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -49,7 +51,7 @@ struct ExtendMaps {
   CUtensorMap vgat;
 };
 
-constexpr int kExtThreads = 256;
+constexpr int kExtThreads = 288;  // 9 warps: K x2, MMA, V x2, softmax x4
 constexpr int kBN = 128;          // kv tokens per tile
 constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
 
@@ -135,11 +137,11 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(o_free + i, 128);
     }
     for (int s = 0; s < C::KS; ++s) {
-      mbar_init(k_full + s, 1);
+      mbar_init(k_full + s, 2);
       mbar_init(k_empty + s, 1);
     }
     for (int s = 0; s < C::VS; ++s) {
-      mbar_init(v_full + s, 1);
+      mbar_init(v_full + s, 2);
       mbar_init(v_empty + s, 1);
     }
     mbar_init(o_done, 1);
@@ -151,9 +153,13 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 3) {
+  if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
     // ------------------------------------------------------------ producers: warp 0 = Q + K, warp 3 = V
-    const bool is_v = warp == 3;
+    // K: warps 0 (rows 0-63, plus Q) and 2 (rows 64-127); V: warps 3 and 8.
+    // Two warps per operand: TMA gather4 ops take warp-uniform operands, so
+    // ptxas issues one lane at a time; splitting rows halves that serial issue.
+    const bool is_v = warp == 3 || warp == 8;
+    const int half = (warp == 2 || warp == 8) ? 1 : 0;
     const int NS = is_v ? C::VS : C::KS;
     uint64_t* full = is_v ? v_full : k_full;
     uint64_t* empty = is_v ? v_empty : k_empty;
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     const CUtensorMap* m_gat = is_v ? &maps.vgat : &maps.kgat;
     const CUtensorMap* m_new = is_v ? &maps.vnew : &maps.knew;
     if (lane == 0) {
-      if (!is_v) tma_prefetch_desc(&maps.q);
+      if (warp == 0) tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(m_new);
       tma_prefetch_desc(m_pool);
       tma_prefetch_desc(m_gat);
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     ExtItem I;
     for (int w = blockIdx.x; w < W; w += gridDim.x) {
       if (!ext_item<TOK>(p, qt, w, I)) continue;
-      if (!is_v) {
+      if (warp == 0) {
         const int qb = it & 1;
         if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
         if (lane == 0) {
@@ -187,38 +193,41 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         const int st = jg % NS, rnd = jg / NS;
         mbar_wait(empty + st, (rnd & 1) ^ 1);
         const uint32_t d = base_s + st * C::KV_BYTES;
-        if (lane == 0) mbar_arrive_expect_tx(full + st, C::KV_BYTES);
+        if (lane == 0) mbar_arrive_expect_tx(full + st, C::KV_BYTES / 2);   // this warp's 64 rows
         __syncwarp();
+        const uint32_t dh = d + half * 64 * kTileRowBytes;                   // rows [half*64, half*64+64)
         if (j < I.n_pre) {
-          const int base = j * kBN + 4 * lane;
+          // lane l: rows half*64 + 4*(l&15) .. +3, column block c = l >> 4
+          const int q4 = lane & 15;
+          const int base = j * kBN + half * 64 + 4 * q4;
           int sl[4];
           bool contig = true;
 #pragma unroll
           for (int i = 0; i < 4; ++i) sl[i] = base + i < I.P ? I.slots[base + i] : -1;
           const int s0 = __shfl_sync(0xffffffffu, sl[0], 0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) contig &= (sl[i] == s0 + 4 * lane + i);
+          for (int i = 0; i < 4; ++i) contig &= (sl[i] == s0 + 4 * q4 + i);
           contig = __all_sync(0xffffffffu, contig);
           if (contig) {
             if (lane == 0) {
 #pragma unroll
               for (int c = 0; c < C::NCB; ++c)
-                tma_load_3d(d + c * kBN * kTileRowBytes, m_pool, full + st, c * 64, I.g, s0);
+                tma_load_3d(dh + c * kBN * kTileRowBytes, m_pool, full + st, c * 64, I.g, s0);
             }
-          } else {
+          } else if ((lane >> 4) < C::NCB) {
+            // one tile::gather4 per lane (4 rows x 64 columns)
+            const int c = lane >> 4;
             int r[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) r[i] = sl[i] > 0 ? sl[i] * p.h_kv + I.g : oob_row;
-#pragma unroll
-            for (int c = 0; c < C::NCB; ++c)
-              tma_gather4(d + c * kBN * kTileRowBytes + 4 * lane * kTileRowBytes, m_gat, full + st, c * 64, r[0],
-                          r[1], r[2], r[3]);
+            tma_gather4(dh + c * kBN * kTileRowBytes + 4 * q4 * kTileRowBytes, m_gat, full + st, c * 64, r[0], r[1],
+                        r[2], r[3]);
           }
         } else if (lane == 0) {
           const int nn = j - I.n_pre;
 #pragma unroll
           for (int c = 0; c < C::NCB; ++c)
-            tma_load_3d(d + c * kBN * kTileRowBytes, m_new, full + st, c * 64, I.g, I.qo + nn * kBN);
+            tma_load_3d(dh + c * kBN * kTileRowBytes, m_new, full + st, c * 64, I.g, I.qo + nn * kBN + half * 64);
         }
       }
       ++it;
@@ -398,25 +407,10 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       jg += I.n_tiles;
       ++it;
     }
-  } else {
-    // ------------------------------------------------------------ warp 2: fused KV store (A5)
-    const int tid = lane;
-    constexpr int VPR = HD / 8;                     // 16-byte vectors per head row
-    ExtItem I;
-    for (int w = blockIdx.x; w < W; w += gridDim.x) {
-      if (!ext_item<TOK>(p, qt, w, I)) continue;
-      const int n_tok = min(I.ext, (I.t + 1) * TOK) - I.t * TOK;
-      for (int idx = tid; idx < n_tok * VPR; idx += 32) {
-        const int i = idx / VPR, c = idx % VPR;
-        const int relp = I.t * TOK + i;
-        const int64_t slot = I.slots[I.P + relp];
-        const int64_t src = (int64_t(I.qo + relp) * p.h_kv + I.g) * HD + c * 8;
-        const int64_t dst = (slot * p.h_kv + I.g) * HD + c * 8;
-        *reinterpret_cast<uint4*>(p.kpool + dst) = *reinterpret_cast<const uint4*>(p.k_new + src);
-        *reinterpret_cast<uint4*>(p.vpool + dst) = *reinterpret_cast<const uint4*>(p.v_new + src);
-      }
-    }
   }
+  // warp 2 only owns the TMEM allocation.  (The new K/V rows are stored into
+  // their slots by extend_store_kernel, launched just before this kernel on
+  // the same stream: this kernel reads new K/V from k_new / v_new directly.)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -475,14 +469,14 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   {
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), N};
     uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
-    uint32_t box[3] = {64, 1, kBN};
+    uint32_t box[3] = {64, 1, kBN / 2};   // one half tile (64 rows) per producer warp
     if (!make_map(&mp.knew, p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
     if (!make_map(&mp.vnew, p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), uint64_t(p.num_slots)};
     uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
-    uint32_t box[3] = {64, 1, kBN};
+    uint32_t box[3] = {64, 1, kBN / 2};
     if (!make_map(&mp.kpool, p.kpool, 3, dims, str, box)) return cudaErrorInvalidValue;
     if (!make_map(&mp.vpool, p.vpool, 3, dims, str, box)) return cudaErrorInvalidValue;
   }

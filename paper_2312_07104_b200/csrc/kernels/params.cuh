@@ -81,6 +81,9 @@ inline size_t decode_ws_bytes(int h_q, int head_dim, int batch, int max_seq_len,
 
 cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
                             void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st);
+cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32_t* qo, const int32_t* ext,
+                                const int32_t* prefix, const int32_t* rows, const int32_t* rtt, int64_t rtt_stride,
+                                const void* k, const void* v, void* kpool, void* vpool, cudaStream_t st);
 cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st, int* launches);
 cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void* q, int64_t total_new, int batch,
                           int max_ext, cudaStream_t st);

@@ -31,6 +31,47 @@ __global__ void __launch_bounds__(256) store_kv_kernel(int64_t n, int row_vec, c
   }
 }
 
+// Extend-side store (A5 of rx_extend): token i of the ragged batch belongs to
+// the request b with qo[b] <= i < qo[b] + ext[b]; its slot is
+// rtt[row_b][prefix[b] + i - qo[b]].  One warp per token row (all local heads,
+// contiguous), 16-byte vectors, every warp independent (no serial chains).
+__global__ void __launch_bounds__(256) extend_store_kernel(
+    int64_t n, int batch, int row_vec, const int32_t* __restrict__ qo, const int32_t* __restrict__ ext,
+    const int32_t* __restrict__ prefix, const int32_t* __restrict__ rows, const int32_t* __restrict__ rtt,
+    int64_t rtt_stride, const int4* __restrict__ k, const int4* __restrict__ v, int4* __restrict__ kpool,
+    int4* __restrict__ vpool) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < n;
+       i += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    int lo = 0, hi = batch - 1;                      // last b with qo[b] <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (qo[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    const int b = lo;
+    const int j = int(i - qo[b]);
+    if (j >= ext[b]) continue;                       // (qo need not be dense)
+    const int row = rows ? rows[b] : b;
+    const int64_t slot = rtt[int64_t(row) * rtt_stride + prefix[b] + j];
+    for (int c = lane; c < row_vec; c += 32) {
+      kpool[slot * row_vec + c] = k[i * row_vec + c];
+      vpool[slot * row_vec + c] = v[i * row_vec + c];
+    }
+  }
+}
+
+cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32_t* qo, const int32_t* ext,
+                                const int32_t* prefix, const int32_t* rows, const int32_t* rtt, int64_t rtt_stride,
+                                const void* k, const void* v, void* kpool, void* vpool, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  extend_store_kernel<<<int(blocks), 256, 0, st>>>(n, batch, row_bytes / 16, qo, ext, prefix, rows, rtt, rtt_stride,
+                                                   static_cast<const int4*>(k), static_cast<const int4*>(v),
+                                                   static_cast<int4*>(kpool), static_cast<int4*>(vpool));
+  return cudaPeekAtLastError();
+}
+
 cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
                             void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
