@@ -302,23 +302,24 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         const uint32_t t_s = tmem + lane_off + (g_ & 1) * 128;
         mbar_wait(s_full + (g_ & 1), (g_ >> 1) & 1);
         tc_fence_after();
-        float sv[kBN];
-#pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) tmem_ld32(t_s + c * 32, sv + c * 32);
-        tmem_ld_wait();
         // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel.
         // Scores stay raw (unscaled); the scale is folded into the exp2 FFMA.
+        // Two passes over 32-column TMEM chunks (max, then exp/pack/store):
+        // TMEM reads are cheap, registers are not (9 warps per CTA).
         const int lim = j < I.n_pre ? I.P - j * kBN - 1 : rel - (j - I.n_pre) * kBN;
         const bool full = __all_sync(0xffffffffu, lim >= kBN - 1);   // warp-uniform
         float mx = -INFINITY;
-        if (full) {
 #pragma unroll
-          for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, sv[c]);
-        } else {
+        for (int c = 0; c < kBN / 32; ++c) {
+          float sv[32];
+          tmem_ld32(t_s + c * 32, sv);
+          tmem_ld_wait();
+          if (full) {
 #pragma unroll
-          for (int c = 0; c < kBN; ++c) {
-            sv[c] = c <= lim ? sv[c] : -INFINITY;
-            mx = fmaxf(mx, sv[c]);
+            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, sv[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, 32 * c + e <= lim ? sv[e] : -INFINITY);
           }
         }
         mx *= p.scale_log2;
@@ -349,31 +350,40 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           l *= corr;
           m_ref = m_new;
         }
-        uint32_t pk[kBN / 2];
         float rs = 0.f;
         const float sc = p.scale_log2, nm = -m_ref;
-        if (full) {
-          // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
-          // every 4th column is evaluated on the FMA pipe instead.
 #pragma unroll
-          for (int c = 0; c < kBN / 2; ++c) {
-            const float x0 = fmaf(sv[2 * c], sc, nm), x1 = fmaf(sv[2 * c + 1], sc, nm);
-            const float e0 = fast_exp2(x0);
-            const float e1 = (c & 1) ? exp2_poly3(x1) : fast_exp2(x1);
-            rs += e0 + e1;
-            pk[c] = pack_bf16(e0, e1);
-          }
-        } else {
+        for (int c = 0; c < kBN / 32; ++c) {
+          // chunk c: S columns 32c..32c+31 -> P (bf16 pairs) columns 16c..16c+15, which lie
+          // at or below columns already read, so the in-place overwrite is safe
+          float sv[32];
+          tmem_ld32(t_s + c * 32, sv);
+          tmem_ld_wait();
+          uint32_t pk[16];
+          if (full) {
+            // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
+            // every 4th column is evaluated on the FMA pipe instead.
 #pragma unroll
-          for (int c = 0; c < kBN / 2; ++c) {
-            const float e0 = fast_exp2(fmaf(sv[2 * c], sc, nm)), e1 = fast_exp2(fmaf(sv[2 * c + 1], sc, nm));
-            rs += e0 + e1;
-            pk[c] = pack_bf16(e0, e1);
+            for (int e = 0; e < 16; ++e) {
+              const float x0 = fmaf(sv[2 * e], sc, nm), x1 = fmaf(sv[2 * e + 1], sc, nm);
+              const float e0 = fast_exp2(x0);
+              const float e1 = (e & 1) ? exp2_poly3(x1) : fast_exp2(x1);
+              rs += e0 + e1;
+              pk[e] = pack_bf16(e0, e1);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int col = 32 * c + 2 * e;
+              const float e0 = col <= lim ? fast_exp2(fmaf(sv[2 * e], sc, nm)) : 0.f;
+              const float e1 = col + 1 <= lim ? fast_exp2(fmaf(sv[2 * e + 1], sc, nm)) : 0.f;
+              rs += e0 + e1;
+              pk[e] = pack_bf16(e0, e1);
+            }
           }
+          tmem_st16(t_s + c * 16, pk);
         }
         l += rs;
-        tmem_st32(t_s, pk);
-        tmem_st32(t_s + 32, pk + 32);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full + (g_ & 1));
