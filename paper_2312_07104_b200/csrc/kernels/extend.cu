@@ -14,10 +14,10 @@
 //  * warp 0 = TMA producer: Q by a 3-D tiled load; new K/V by 3-D tiled
 //    loads; cached-prefix K/V either by one 3-D tiled load per 64 columns when
 //    the 128 slots of the tile are consecutive (the smallest-first allocator
-//    makes that the common case), or by cp.async.bulk.tensor tile::gather4
-//    (4 pool rows per instruction, issued by all 32 lanes) otherwise; all into
-//    128B-swizzled smem; separate K (3-deep) and V (2-deep) rings with
-//    full/empty mbarriers;
+//    makes that common for prompt tokens), or by per-lane 16-byte cp.async
+//    gathers into the swizzled layout otherwise (decode-time slots interleave
+//    requests); separate K (3-deep) and V (2-deep) rings with full/empty
+//    mbarriers;
 //  * warp 1 = single-thread UMMA issuer: S = Q K^T (bf16 -> fp32 TMEM,
 //    double-buffered) then O += P V with P read from TMEM (A operand in
 //    tensor memory), all 128x128 / 128xHD tiles, cta_group::1;
@@ -26,9 +26,8 @@
 //    rescaling (only when the running max grows by > 8), P packed to bf16 and
 //    tcgen05.st over the S columns; epilogue O / l -> bf16 -> global;
 //  * warp 2: TMEM allocation; warp 3: V producer (K and V rings are separate).
-//  * A5 (store new K/V into their slots) runs as a separate, fully parallel
-//    kernel just before on the same stream (store.cu): inside this kernel it
-//    was a latency-bound serial copy on one warp that outlived short items.
+//  * A5 (store new K/V into their slots) is a separate, fully parallel kernel
+//    launched just before on the same stream (store.cu).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -47,11 +46,9 @@ struct ExtendMaps {
   CUtensorMap vnew;
   CUtensorMap kpool;   // 3D (HD, h_kv, S)  box (64, 1, 128)
   CUtensorMap vpool;
-  CUtensorMap kgat;    // 2D (HD, S*h_kv)   box (64, 1)  gather4
-  CUtensorMap vgat;
 };
 
-constexpr int kExtThreads = 288;  // 9 warps: K x2, MMA, V x2, softmax x4
+constexpr int kExtThreads = 256;
 constexpr int kBN = 128;          // kv tokens per tile
 constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
 
@@ -137,11 +134,11 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(o_free + i, 128);
     }
     for (int s = 0; s < C::KS; ++s) {
-      mbar_init(k_full + s, 2);
+      mbar_init(k_full + s, 32);   // all producer lanes arrive (TMA: 1 expect_tx + 31; cp.async: 32 noinc)
       mbar_init(k_empty + s, 1);
     }
     for (int s = 0; s < C::VS; ++s) {
-      mbar_init(v_full + s, 2);
+      mbar_init(v_full + s, 32);
       mbar_init(v_empty + s, 1);
     }
     mbar_init(o_done, 1);
@@ -153,32 +150,26 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
+  if (warp == 0 || warp == 3) {
     // ------------------------------------------------------------ producers: warp 0 = Q + K, warp 3 = V
-    // K: warps 0 (rows 0-63, plus Q) and 2 (rows 64-127); V: warps 3 and 8.
-    // Two warps per operand: TMA gather4 ops take warp-uniform operands, so
-    // ptxas issues one lane at a time; splitting rows halves that serial issue.
-    const bool is_v = warp == 3 || warp == 8;
-    const int half = (warp == 2 || warp == 8) ? 1 : 0;
+    const bool is_v = warp == 3;
     const int NS = is_v ? C::VS : C::KS;
     uint64_t* full = is_v ? v_full : k_full;
     uint64_t* empty = is_v ? v_empty : k_empty;
     const uint32_t base_s = is_v ? sv_ : sk;
     const CUtensorMap* m_pool = is_v ? &maps.vpool : &maps.kpool;
-    const CUtensorMap* m_gat = is_v ? &maps.vgat : &maps.kgat;
+    const __nv_bfloat16* base_g = is_v ? p.vpool : p.kpool;
     const CUtensorMap* m_new = is_v ? &maps.vnew : &maps.knew;
     if (lane == 0) {
-      if (warp == 0) tma_prefetch_desc(&maps.q);
+      if (!is_v) tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(m_new);
       tma_prefetch_desc(m_pool);
-      tma_prefetch_desc(m_gat);
     }
-    const int oob_row = int(p.num_slots * p.h_kv);  // coordinate past the end: TMA zero-fills
     int it = 0, jg = 0;
     ExtItem I;
     for (int w = blockIdx.x; w < W; w += gridDim.x) {
       if (!ext_item<TOK>(p, qt, w, I)) continue;
-      if (warp == 0) {
+      if (!is_v) {
         const int qb = it & 1;
         if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
         if (lane == 0) {
@@ -193,41 +184,58 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         const int st = jg % NS, rnd = jg / NS;
         mbar_wait(empty + st, (rnd & 1) ^ 1);
         const uint32_t d = base_s + st * C::KV_BYTES;
-        if (lane == 0) mbar_arrive_expect_tx(full + st, C::KV_BYTES / 2);   // this warp's 64 rows
-        __syncwarp();
-        const uint32_t dh = d + half * 64 * kTileRowBytes;                   // rows [half*64, half*64+64)
+        // prefix tile: one 3-D TMA box when its 128 slots are consecutive, else a
+        // cp.async gather (see below); new-KV tile: one 3-D TMA box
+        bool tma = true;
+        int s0 = 0;
         if (j < I.n_pre) {
-          // lane l: rows half*64 + 4*(l&15) .. +3, column block c = l >> 4
-          const int q4 = lane & 15;
-          const int base = j * kBN + half * 64 + 4 * q4;
-          int sl[4];
+          const int base = j * kBN + 4 * lane;
           bool contig = true;
+          s0 = I.slots[j * kBN];                        // (j*kBN < P: the tile has >= 1 cached row)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) sl[i] = base + i < I.P ? I.slots[base + i] : -1;
-          const int s0 = __shfl_sync(0xffffffffu, sl[0], 0);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) contig &= (sl[i] == s0 + 4 * q4 + i);
-          contig = __all_sync(0xffffffffu, contig);
-          if (contig) {
-            if (lane == 0) {
+          for (int i = 0; i < 4; ++i) contig &= base + i < I.P && I.slots[base + i] == s0 + 4 * lane + i;
+          tma = __all_sync(0xffffffffu, contig);
+        }
+        if (tma) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(full + st, C::KV_BYTES);
+            if (j < I.n_pre) {
 #pragma unroll
               for (int c = 0; c < C::NCB; ++c)
-                tma_load_3d(dh + c * kBN * kTileRowBytes, m_pool, full + st, c * 64, I.g, s0);
+                tma_load_3d(d + c * kBN * kTileRowBytes, m_pool, full + st, c * 64, I.g, s0);
+            } else {
+              const int nn = j - I.n_pre;
+#pragma unroll
+              for (int c = 0; c < C::NCB; ++c)
+                tma_load_3d(d + c * kBN * kTileRowBytes, m_new, full + st, c * 64, I.g, I.qo + nn * kBN);
             }
-          } else if ((lane >> 4) < C::NCB) {
-            // one tile::gather4 per lane (4 rows x 64 columns)
-            const int c = lane >> 4;
-            int r[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) r[i] = sl[i] > 0 ? sl[i] * p.h_kv + I.g : oob_row;
-            tma_gather4(dh + c * kBN * kTileRowBytes + 4 * q4 * kTileRowBytes, m_gat, full + st, c * 64, r[0], r[1],
-                        r[2], r[3]);
+          } else {
+            mbar_arrive(full + st);
           }
-        } else if (lane == 0) {
-          const int nn = j - I.n_pre;
+        } else {
+          // Fragmented slots: per-lane 16-byte cp.async gathers written straight
+          // into the 128B-swizzled layout (chunk k of row r -> chunk k ^ (r & 7)).
+          // CPR lanes cover one pool row; rows past the prefix are zero-filled.
+          // (TMA tile::gather4 takes warp-uniform operands, which ptxas issues one
+          // lane at a time; this path keeps all 32 lanes issuing.)
+          constexpr int CPR = HD / 8, RPI = 32 / CPR;
+          const int ch = lane % CPR, rsub = lane / CPR;
+          const uint32_t dcol = d + (ch >> 3) * kBN * kTileRowBytes;
+          int slot_r[4];                                // slots of rows lane, lane+32, lane+64, lane+96
 #pragma unroll
-          for (int c = 0; c < C::NCB; ++c)
-            tma_load_3d(dh + c * kBN * kTileRowBytes, m_new, full + st, c * 64, I.g, I.qo + nn * kBN + half * 64);
+          for (int i = 0; i < 4; ++i) {
+            const int pos = j * kBN + lane + 32 * i;
+            slot_r[i] = pos < I.P ? I.slots[pos] : -1;
+          }
+#pragma unroll
+          for (int rr = 0; rr < kBN; rr += RPI) {
+            const int row = rr + rsub;
+            const int sl = __shfl_sync(0xffffffffu, slot_r[rr / 32], row & 31);
+            const bool ok = sl > 0;
+            const __nv_bfloat16* src = base_g + (int64_t(ok ? sl : 0) * p.h_kv + I.g) * HD + ch * 8;
+            cp_async_16(dcol + row * kTileRowBytes + (((ch & 7) ^ (row & 7)) << 4), src, ok ? 16u : 0u);
+          }
+          cp_async_mbar_arrive_noinc(full + st);
         }
       }
       ++it;
@@ -251,6 +259,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           const int st = g_ % C::KS;
           mbar_wait(k_full + st, (g_ / C::KS) & 1);
           tc_fence_after();
+          fence_proxy_async();   // cp.async (generic-proxy) writes -> visible to the MMA (async proxy)
           const uint32_t kb = sk + st * C::KV_BYTES;
           const uint32_t t_s = tmem + (g_ & 1) * 128;
 #pragma unroll
@@ -271,6 +280,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           tc_fence_after();
           const int st = g_ % C::VS;
           mbar_wait(v_full + st, (g_ / C::VS) & 1);
+          fence_proxy_async();
           const uint32_t vb = sv_ + st * C::KV_BYTES;
           const uint32_t t_p = tmem + (g_ & 1) * 128;
 #pragma unroll
@@ -302,24 +312,23 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         const uint32_t t_s = tmem + lane_off + (g_ & 1) * 128;
         mbar_wait(s_full + (g_ & 1), (g_ >> 1) & 1);
         tc_fence_after();
+        float sv[kBN];
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c) tmem_ld32(t_s + c * 32, sv + c * 32);
+        tmem_ld_wait();
         // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel.
         // Scores stay raw (unscaled); the scale is folded into the exp2 FFMA.
-        // Two passes over 32-column TMEM chunks (max, then exp/pack/store):
-        // TMEM reads are cheap, registers are not (9 warps per CTA).
         const int lim = j < I.n_pre ? I.P - j * kBN - 1 : rel - (j - I.n_pre) * kBN;
         const bool full = __all_sync(0xffffffffu, lim >= kBN - 1);   // warp-uniform
         float mx = -INFINITY;
+        if (full) {
 #pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {
-          float sv[32];
-          tmem_ld32(t_s + c * 32, sv);
-          tmem_ld_wait();
-          if (full) {
+          for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, sv[c]);
+        } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, sv[e]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, 32 * c + e <= lim ? sv[e] : -INFINITY);
+          for (int c = 0; c < kBN; ++c) {
+            sv[c] = c <= lim ? sv[c] : -INFINITY;
+            mx = fmaxf(mx, sv[c]);
           }
         }
         mx *= p.scale_log2;
@@ -350,40 +359,31 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           l *= corr;
           m_ref = m_new;
         }
+        uint32_t pk[kBN / 2];
         float rs = 0.f;
         const float sc = p.scale_log2, nm = -m_ref;
+        if (full) {
+          // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
+          // every 4th column is evaluated on the FMA pipe instead.
 #pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {
-          // chunk c: S columns 32c..32c+31 -> P (bf16 pairs) columns 16c..16c+15, which lie
-          // at or below columns already read, so the in-place overwrite is safe
-          float sv[32];
-          tmem_ld32(t_s + c * 32, sv);
-          tmem_ld_wait();
-          uint32_t pk[16];
-          if (full) {
-            // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
-            // every 4th column is evaluated on the FMA pipe instead.
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const float x0 = fmaf(sv[2 * e], sc, nm), x1 = fmaf(sv[2 * e + 1], sc, nm);
-              const float e0 = fast_exp2(x0);
-              const float e1 = (e & 1) ? exp2_poly3(x1) : fast_exp2(x1);
-              rs += e0 + e1;
-              pk[e] = pack_bf16(e0, e1);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int col = 32 * c + 2 * e;
-              const float e0 = col <= lim ? fast_exp2(fmaf(sv[2 * e], sc, nm)) : 0.f;
-              const float e1 = col + 1 <= lim ? fast_exp2(fmaf(sv[2 * e + 1], sc, nm)) : 0.f;
-              rs += e0 + e1;
-              pk[e] = pack_bf16(e0, e1);
-            }
+          for (int c = 0; c < kBN / 2; ++c) {
+            const float x0 = fmaf(sv[2 * c], sc, nm), x1 = fmaf(sv[2 * c + 1], sc, nm);
+            const float e0 = fast_exp2(x0);
+            const float e1 = (c & 1) ? exp2_poly3(x1) : fast_exp2(x1);
+            rs += e0 + e1;
+            pk[c] = pack_bf16(e0, e1);
           }
-          tmem_st16(t_s + c * 16, pk);
+        } else {
+#pragma unroll
+          for (int c = 0; c < kBN / 2; ++c) {
+            const float e0 = fast_exp2(fmaf(sv[2 * c], sc, nm)), e1 = fast_exp2(fmaf(sv[2 * c + 1], sc, nm));
+            rs += e0 + e1;
+            pk[c] = pack_bf16(e0, e1);
+          }
         }
         l += rs;
+        tmem_st32(t_s, pk);
+        tmem_st32(t_s + 32, pk + 32);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full + (g_ & 1));
@@ -418,8 +418,8 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       ++it;
     }
   }
-  // warp 2 only owns the TMEM allocation.  (The new K/V rows are stored into
-  // their slots by extend_store_kernel, launched just before this kernel on
+  // warp 2 only owns the TMEM allocation.  (A5, storing the new K/V rows into
+  // their slots, is extend_store_kernel, launched just before this kernel on
   // the same stream: this kernel reads new K/V from k_new / v_new directly.)
   tc_fence_before();
   __syncthreads();
@@ -479,23 +479,16 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   {
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), N};
     uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
-    uint32_t box[3] = {64, 1, kBN / 2};   // one half tile (64 rows) per producer warp
+    uint32_t box[3] = {64, 1, kBN};
     if (!make_map(&mp.knew, p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
     if (!make_map(&mp.vnew, p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), uint64_t(p.num_slots)};
     uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
-    uint32_t box[3] = {64, 1, kBN / 2};
+    uint32_t box[3] = {64, 1, kBN};
     if (!make_map(&mp.kpool, p.kpool, 3, dims, str, box)) return cudaErrorInvalidValue;
     if (!make_map(&mp.vpool, p.vpool, 3, dims, str, box)) return cudaErrorInvalidValue;
-  }
-  {
-    uint64_t dims[2] = {hd, uint64_t(p.num_slots) * uint64_t(p.h_kv)};
-    uint64_t str[1] = {hd * 2};
-    uint32_t box[2] = {64, 1};
-    if (!make_map(&mp.kgat, p.kpool, 2, dims, str, box)) return cudaErrorInvalidValue;
-    if (!make_map(&mp.vgat, p.vpool, 2, dims, str, box)) return cudaErrorInvalidValue;
   }
   static bool attr = false;
   if (!attr) {

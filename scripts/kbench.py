@@ -83,6 +83,9 @@ def main():
                 rtt[b, P:] = torch.arange(P + 1 + b * E, P + 1 + (b + 1) * E)
             else:
                 rtt[b] = torch.arange(1 + b * (P + E), 1 + (b + 1) * (P + E))
+        if a.scatter:   # fragmented prefix slots (every tile takes the tile::gather4 path)
+            pre = rtt[:, :P].reshape(-1)
+            rtt[:, :P] = pre[torch.randperm(pre.numel(), device=dev, generator=g)].view(B, P)
         N = B * E
         q = torch.randn((N, h_q, hd), device=dev, generator=g).to(torch.bfloat16)
         kn = torch.randn((N, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
