@@ -269,6 +269,27 @@ rx_status rx_decode_append(const rx_attn_cfg* cfg, int32_t batch,
 
 size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len);
 
+/* Shared-prefix ("cascade") decode step — SURVEY §8(f) NEXT-1, motivated by
+ * "requests with the same prompt prefix can reuse the KV cache" (P:171 [§3])
+ * and the shared-prefix kernels cited at P:458 [§7].  Same result as
+ * rx_decode_append, but positions [0, shared_len), which must hold the SAME
+ * slots in every batch row (a radix node all requests are pinned on; the slots
+ * of row d_rows[0] are read), are attended ONCE for the whole batch as a dense
+ * tensor-core problem (rows = requests x GQA heads, split over the prefix),
+ * each request's suffix [shared_len, seq_len) by the decode kernel, and the
+ * partials merged by log-sum-exp.  Requires 0 <= shared_len < every seq_len
+ * (shared_len == 0 falls back to rx_decode_append).  3 launches.
+ * Workspace: rx_decode_cascade_workspace_bytes(cfg, batch, max_seq_len, shared_len). */
+rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch,
+                                   int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
+                                   const int32_t* d_seq_lens, int32_t max_seq_len, int32_t shared_len,
+                                   const void* d_q, const void* d_k_new, const void* d_v_new,
+                                   const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
+                                   int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream);
+
+size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len,
+                                         int32_t shared_len);
+
 /* Number of kernel launches the last successful rx_extend / rx_decode /
  * rx_store_kv call on this thread issued (for launch accounting). */
 int32_t rx_last_launch_count(void);

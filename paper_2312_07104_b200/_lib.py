@@ -59,6 +59,9 @@ SIGNATURES = {
     "rx_decode_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, i64,
                                    vp, vp, sz, vp]),
     "rx_decode_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
+    "rx_decode_cascade_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, i32, vp, vp, vp, vp, vp,
+                                           vp, i64, vp, vp, sz, vp]),
+    "rx_decode_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32, i32]),
     "rx_last_launch_count": (i32, []),
 }
 

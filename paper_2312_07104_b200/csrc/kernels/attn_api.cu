@@ -125,6 +125,93 @@ rx_status rx_decode_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt
                      num_slots, d_o, d_ws, ws_bytes, stream, d_k_new, d_v_new, d_new_slots, d_rtt);
 }
 
+size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len,
+                                         int32_t shared_len) {
+  if (check_cfg(cfg) != RX_OK || batch <= 0 || shared_len <= 0 || max_seq_len <= shared_len) return 0;
+  return rx::cascade_ws_bytes(cfg->h_q, cfg->head_dim, batch, cfg->h_kv, max_seq_len, shared_len);
+}
+
+rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
+                                   const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len,
+                                   int32_t shared_len, const void* d_q, const void* d_k_new, const void* d_v_new,
+                                   const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool, int64_t num_slots,
+                                   void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
+  rx_status s = check_cfg(cfg);
+  if (s != RX_OK) return s;
+  if (batch < 0 || num_slots < 1 || shared_len < 0) return RX_E_INVALID;
+  g_last_launches = 0;
+  if (batch == 0) return RX_OK;
+  if (shared_len == 0)   // nothing shared: the ordinary fused path
+    return rx_decode_append(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_new, d_v_new,
+                            d_new_slots, d_k_pool, d_v_pool, num_slots, d_o, d_ws, ws_bytes, stream);
+  if (max_seq_len <= shared_len || !d_rtt || !d_seq_lens || !d_q || !d_k_new || !d_v_new || !d_new_slots ||
+      !d_k_pool || !d_v_pool || !d_o || rtt_stride < max_seq_len)
+    return RX_E_INVALID;
+  const int G = cfg->h_q / cfg->h_kv;
+  const size_t need = rx::cascade_ws_bytes(cfg->h_q, cfg->head_dim, batch, cfg->h_kv, max_seq_len, shared_len);
+  if (!d_ws || ws_bytes < need) return RX_E_WORKSPACE;
+  const rx::CascadePlan pl = rx::plan_cascade(batch, cfg->h_kv, G, max_seq_len, shared_len);
+  const size_t n = size_t(batch) * cfg->h_q * pl.total_splits;
+  float* ws_o = static_cast<float*>(d_ws);
+  float* ws_lse = reinterpret_cast<float*>(static_cast<char*>(d_ws) + n * cfg->head_dim * sizeof(float));
+  const float scale_log2 = cfg->sm_scale * 1.4426950408889634f;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  // (1) suffix [shared_len, seq_len) + the step's KV append: partials at split >= n_sh
+  rx::DecodeParams dp{};
+  dp.q = static_cast<const __nv_bfloat16*>(d_q);
+  dp.kpool = static_cast<const __nv_bfloat16*>(d_k_pool);
+  dp.vpool = static_cast<const __nv_bfloat16*>(d_v_pool);
+  dp.o = static_cast<__nv_bfloat16*>(d_o);
+  dp.rtt = d_rtt;
+  dp.rtt_stride = rtt_stride;
+  dp.rows = d_rows;
+  dp.seq_lens = d_seq_lens;
+  dp.ws_o = ws_o;
+  dp.ws_lse = ws_lse;
+  dp.h_q = cfg->h_q;
+  dp.h_kv = cfg->h_kv;
+  dp.chunk = pl.suffix.chunk;
+  dp.max_splits = pl.total_splits;
+  dp.scale_log2 = scale_log2;
+  dp.k_new = static_cast<const __nv_bfloat16*>(d_k_new);
+  dp.v_new = static_cast<const __nv_bfloat16*>(d_v_new);
+  dp.new_slots = d_new_slots;
+  dp.rtt_w = d_rtt;
+  dp.kv_start = shared_len;
+  dp.split_base = pl.n_sh;
+  int launches = 0;
+  cudaError_t e = rx::launch_decode(cfg->head_dim, G, dp, batch, st, &launches);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  // (2) shared prefix [0, shared_len), attended ONCE for all requests on the
+  //     tensor cores (rows = requests x GQA heads): partials at splits [0, n_sh)
+  rx::ExtendParams ep{};
+  ep.rtt = d_rtt;
+  ep.rtt_stride = rtt_stride;
+  ep.rows = d_rows;
+  ep.kpool = static_cast<__nv_bfloat16*>(d_k_pool);
+  ep.vpool = static_cast<__nv_bfloat16*>(d_v_pool);
+  ep.h_q = cfg->h_q;
+  ep.h_kv = cfg->h_kv;
+  ep.num_slots = num_slots;
+  ep.scale_log2 = scale_log2;
+  ep.cascade = 1;
+  ep.kv_split_tiles = pl.kv_split_tiles;
+  ep.n_kv_splits = pl.n_sh;
+  ep.part_o = ws_o;
+  ep.part_lse = ws_lse;
+  ep.part_splits = pl.total_splits;
+  ep.part_base = 0;
+  ep.cas_prefix = shared_len;
+  e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, batch, st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  // (3) log-sum-exp merge of shared + suffix partials
+  e = rx::launch_decode_merge(cfg->head_dim, dp, batch, st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  g_last_launches = launches + 2;
+  return RX_OK;
+}
+
 size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len) {
   (void)cfg;
   (void)batch;

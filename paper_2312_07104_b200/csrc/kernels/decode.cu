@@ -68,10 +68,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   extern __shared__ __align__(128) uint8_t smem[];
   const int b = blockIdx.z, g = blockIdx.y, s = blockIdx.x;
   const int L = p.seq_lens[b];
-  const int start = s * p.chunk;
+  const int start = p.kv_start + s * p.chunk;      // kv_start > 0: cascade (shared prefix elsewhere)
   if (start >= L) return;
   const int end = min(L, start + p.chunk);
-  const int nsplit = (L + p.chunk - 1) / p.chunk;
+  const int nsplit = (L - p.kv_start + p.chunk - 1) / p.chunk;
   const int row = p.rows ? p.rows[b] : b;
   const int32_t* slots = p.rtt + int64_t(row) * p.rtt_stride;
 
@@ -245,10 +245,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
       acc += f * opart[(w * HD + d) * 8 + h];
     }
     const int hq = g * G + h;
-    if (nsplit == 1) {
+    if (nsplit == 1 && p.split_base == 0) {
       p.o[(int64_t(b) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / Ls);
     } else {
-      const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits + s;
+      const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits + p.split_base + s;
       p.ws_o[base * HD + d] = acc / Ls;
       if (d == 0) p.ws_lse[base] = M + __log2f(Ls);
     }
@@ -260,7 +260,7 @@ template <int HD>
 __global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p) {
   const int b = blockIdx.x, hq = blockIdx.y;
   const int L = p.seq_lens[b];
-  const int nsplit = (L + p.chunk - 1) / p.chunk;
+  const int nsplit = p.split_base + (L - p.kv_start + p.chunk - 1) / p.chunk;
   if (nsplit <= 1) return;
   const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits;
   float M = -INFINITY;
@@ -282,13 +282,19 @@ static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_
     cudaFuncSetAttribute(decode_kernel<HD, G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  dim3 grid(p.max_splits, p.h_kv, batch);
+  dim3 grid(p.max_splits - p.split_base, p.h_kv, batch);   // suffix splits (cascade: shared partials come first)
   decode_kernel<HD, G, STAGES><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);
   *launches = 1;
-  if (p.max_splits > 1) {
+  if (p.max_splits > 1 && p.split_base == 0) {   // cascade: the caller merges after the shared part
     decode_merge_kernel<HD><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
     *launches = 2;
   }
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st) {
+  if (head_dim == 64) decode_merge_kernel<64><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
+  else decode_merge_kernel<128><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
   return cudaPeekAtLastError();
 }
 

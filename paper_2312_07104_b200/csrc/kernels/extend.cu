@@ -72,6 +72,8 @@ struct ExtCfg {
 // CTAs round-robin; every role of a CTA walks the same list.
 struct ExtItem {
   int b, g, t, P, ext, qo, n_pre, n_tiles;
+  int tile0;            // first prefix tile (cascade chunk), 0 otherwise
+  int split;            // cascade chunk index
   const int32_t* slots;
 };
 
@@ -80,6 +82,28 @@ __device__ __forceinline__ bool ext_item(const ExtendParams& p, int qt, int w, E
   // (request, kv head) outer, q tile inner (heaviest first): the q tiles of
   // one (b, g) run on neighbouring CTAs at the same time, so that head's
   // cached prefix is read from HBM once and re-served from L2.
+  if (p.cascade) {
+    // (kv head, prefix chunk) outer, q tile inner: all q tiles of one chunk
+    // share its K/V through L2.  One virtual request (b = 0) of `batch` rows.
+    const int gs = w / qt;
+    it.t = qt - 1 - w % qt;
+    it.g = gs % p.h_kv;
+    it.split = gs / p.h_kv;
+    it.b = 0;
+    it.ext = p.batch;
+    if (it.t * TOK >= it.ext) return false;
+    it.P = p.cas_prefix;
+    it.qo = 0;
+    const int row = p.rows ? p.rows[0] : 0;
+    it.slots = p.rtt + int64_t(row) * p.rtt_stride;
+    const int total = (it.P + kBN - 1) / kBN;
+    it.tile0 = it.split * p.kv_split_tiles;
+    it.n_pre = min(p.kv_split_tiles, total - it.tile0);
+    it.n_tiles = it.n_pre;
+    return it.n_pre > 0;
+  }
+  it.tile0 = 0;
+  it.split = 0;
   const int bg = w / qt;
   it.t = qt - 1 - w % qt;
   it.g = bg % p.h_kv;
@@ -121,7 +145,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const int qt = p.max_qtiles;
-  const int W = qt * p.h_kv * p.batch;
+  const int W = p.cascade ? qt * p.h_kv * p.n_kv_splits : qt * p.h_kv * p.batch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -188,10 +212,11 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         // cp.async gather (see below); new-KV tile: one 3-D TMA box
         bool tma = true;
         int s0 = 0;
+        const int jt = I.tile0 + j;                     // absolute prefix tile (cascade chunks)
         if (j < I.n_pre) {
-          const int base = j * kBN + 4 * lane;
+          const int base = jt * kBN + 4 * lane;
           bool contig = true;
-          s0 = I.slots[j * kBN];                        // (j*kBN < P: the tile has >= 1 cached row)
+          s0 = I.slots[jt * kBN];                       // (jt*kBN < P: the tile has >= 1 cached row)
 #pragma unroll
           for (int i = 0; i < 4; ++i) contig &= base + i < I.P && I.slots[base + i] == s0 + 4 * lane + i;
           tma = __all_sync(0xffffffffu, contig);
@@ -224,7 +249,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           int slot_r[4];                                // slots of rows lane, lane+32, lane+64, lane+96
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int pos = j * kBN + lane + 32 * i;
+            const int pos = jt * kBN + lane + 32 * i;
             slot_r[i] = pos < I.P ? I.slots[pos] : -1;
           }
 #pragma unroll
@@ -318,7 +343,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         tmem_ld_wait();
         // mask: prefix tile -> col < P - j*BN ; new tile -> nn*BN + col <= rel.
         // Scores stay raw (unscaled); the scale is folded into the exp2 FFMA.
-        const int lim = j < I.n_pre ? I.P - j * kBN - 1 : rel - (j - I.n_pre) * kBN;
+        const int lim = j < I.n_pre ? I.P - (I.tile0 + j) * kBN - 1 : rel - (j - I.n_pre) * kBN;
         const bool full = __all_sync(0xffffffffu, lim >= kBN - 1);   // warp-uniform
         float mx = -INFINITY;
         if (full) {
@@ -399,7 +424,17 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         float ov[32];
         tmem_ld32(t_o + c * 32, ov);
         tmem_ld_wait();
-        if (rel < I.ext) {
+        if (p.cascade) {
+          // partial over this prefix chunk: normalized fp32 o + log2-domain lse
+          if (rel < I.ext) {
+            const int64_t pr = (int64_t(rel) * p.h_q + I.g * G + h) * p.part_splits + p.part_base + I.split;
+            float4* dst = reinterpret_cast<float4*>(p.part_o + pr * HD + c * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              dst[e] = make_float4(ov[4 * e] * inv, ov[4 * e + 1] * inv, ov[4 * e + 2] * inv, ov[4 * e + 3] * inv);
+            if (c == 0) p.part_lse[pr] = m_ref + __log2f(l);
+          }
+        } else if (rel < I.ext) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -465,6 +500,8 @@ static bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t*
 template <int HD, int G>
 static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t total_new, int batch,
                                    int max_ext, cudaStream_t st) {
+  // cascade mode: `batch` virtual rows (decode queries), one virtual request; no
+  // new tiles (the k_new / v_new maps are encoded over the pools, never used)
   using C = ExtCfg<HD>;
   constexpr int TOK = 128 / G;
   ExtendMaps mp;
@@ -480,8 +517,8 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), N};
     uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
     uint32_t box[3] = {64, 1, kBN};
-    if (!make_map(&mp.knew, p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
-    if (!make_map(&mp.vnew, p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.knew, p.cascade ? p.kpool : p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.vnew, p.cascade ? p.vpool : p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), uint64_t(p.num_slots)};
@@ -498,7 +535,7 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   ExtendParams pp = p;
   pp.batch = batch;
   pp.max_qtiles = (max_ext + TOK - 1) / TOK;
-  const int64_t items = int64_t(pp.max_qtiles) * p.h_kv * batch;
+  const int64_t items = int64_t(pp.max_qtiles) * p.h_kv * (p.cascade ? p.n_kv_splits : batch);
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -508,6 +545,17 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   const int grid = int(items < sms ? items : sms);   // persistent: one CTA per SM
   extend_kernel<HD, G><<<grid, kExtThreads, C::SMEM, st>>>(pp, mp);
   return cudaPeekAtLastError();
+}
+
+cudaError_t launch_extend_cascade(int head_dim, int G, const ExtendParams& p, const void* q, int batch,
+                                  cudaStream_t st) {
+  if (batch <= 0 || p.cas_prefix <= 0) return cudaSuccess;
+#define RX_EXT_CASE(HD_, G_) \
+  if (head_dim == HD_ && G == G_) return launch_extend_t<HD_, G_>(p, q, batch, batch, batch, st);
+  RX_EXT_CASE(64, 1) RX_EXT_CASE(64, 2) RX_EXT_CASE(64, 4) RX_EXT_CASE(64, 8)
+  RX_EXT_CASE(128, 1) RX_EXT_CASE(128, 2) RX_EXT_CASE(128, 4) RX_EXT_CASE(128, 8)
+#undef RX_EXT_CASE
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void* q, int64_t total_new, int batch,

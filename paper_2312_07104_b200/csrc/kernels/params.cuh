@@ -31,6 +31,12 @@ struct DecodeParams {
   const __nv_bfloat16* v_new;
   const int32_t* new_slots;
   int32_t* rtt_w;
+  // cascade: positions [0, kv_start) are attended elsewhere (shared prefix);
+  // this kernel covers [kv_start, seq_len) and always writes partials at split
+  // index split_base + s of a [B, h_q, max_splits] layout (max_splits includes
+  // the split_base shared partials); the merge combines split_base + nsplit_b.
+  int kv_start;
+  int split_base;
 };
 
 struct ExtendParams {
@@ -50,6 +56,20 @@ struct ExtendParams {
   float scale_log2;
   int batch;                    // set by the launcher
   int max_qtiles;               // set by the launcher
+  // Cascade (shared-prefix) mode: the `batch` rows are decode queries of B requests
+  // that share cached prefix positions [0, prefix_lens[0]) (slots of table row
+  // rows[0]); no new tiles, no causal mask.  The prefix is cut into n_kv_splits
+  // chunks of kv_split_tiles tiles; each (q tile, kv head, chunk) item writes a
+  // normalized fp32 partial o and its log2-domain lse at split index
+  // part_base + chunk of the [B, h_q, part_splits] partial arrays.
+  int cascade;
+  int kv_split_tiles;
+  int n_kv_splits;
+  float* part_o;                // [B, h_q, part_splits, HD]
+  float* part_lse;              // [B, h_q, part_splits]
+  int part_splits;
+  int part_base;
+  int cas_prefix;               // shared prefix length (cascade mode; prefix_lens unused)
 };
 
 struct DecodePlan {
@@ -79,11 +99,46 @@ inline size_t decode_ws_bytes(int h_q, int head_dim, int batch, int max_seq_len,
   return n * head_dim * sizeof(float) + n * sizeof(float) + 256;
 }
 
+// Cascade plan (shared-prefix decode): the shared prefix [0, shared_len) is cut
+// into n_sh chunks of kv_split_tiles 128-token tiles so that (q tiles x kv heads
+// x chunks) gives ~2 items per SM of a 148-SM part (a constant, not the device's
+// count); the suffix [shared_len, seq_len) follows the ordinary split plan.
+struct CascadePlan {
+  int n_sh;
+  int kv_split_tiles;
+  DecodePlan suffix;
+  int total_splits;
+};
+
+inline CascadePlan plan_cascade(int batch, int h_kv, int group, int max_seq_len, int shared_len) {
+  CascadePlan c{};
+  const int tok = 128 / group;
+  const int qt = (batch + tok - 1) / tok;
+  const int tiles = (shared_len + 127) / 128;
+  const int per_chunk = qt * h_kv;
+  int n = (2 * 148 + per_chunk - 1) / per_chunk;
+  n = n < 1 ? 1 : (n > tiles ? tiles : n);
+  c.kv_split_tiles = (tiles + n - 1) / n;
+  c.n_sh = (tiles + c.kv_split_tiles - 1) / c.kv_split_tiles;
+  c.suffix = plan_decode(batch, h_kv, max_seq_len - shared_len);
+  c.total_splits = c.n_sh + c.suffix.max_splits;
+  return c;
+}
+
+inline size_t cascade_ws_bytes(int h_q, int head_dim, int batch, int h_kv, int max_seq_len, int shared_len) {
+  CascadePlan c = plan_cascade(batch, h_kv, h_q / h_kv, max_seq_len, shared_len);
+  const size_t n = size_t(batch) * h_q * c.total_splits;
+  return n * head_dim * sizeof(float) + n * sizeof(float) + 256;
+}
+
 cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
                             void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st);
 cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32_t* qo, const int32_t* ext,
                                 const int32_t* prefix, const int32_t* rows, const int32_t* rtt, int64_t rtt_stride,
                                 const void* k, const void* v, void* kpool, void* vpool, cudaStream_t st);
+cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st);
+cudaError_t launch_extend_cascade(int head_dim, int G, const ExtendParams& p, const void* q, int batch,
+                                  cudaStream_t st);
 cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st, int* launches);
 cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void* q, int64_t total_new, int batch,
                           int max_ext, cudaStream_t st);

@@ -281,6 +281,69 @@ def test_extend_many_items_ragged(h_q, h_kv, hd):
 @pytest.mark.parametrize("h_q,h_kv,hd,lens", [(32, 8, 128, [1, 40, 700, 3000]), (8, 2, 64, [2, 300]),
                                               (64, 8, 128, [8300, 5])])
 def test_decode_append_equals_store_then_decode(h_q, h_kv, hd, lens):
+    _decode_append_check(h_q, h_kv, hd, lens)
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,B,shared,contig", [
+    (64, 8, 128, 128, 8192, True),     # C5 shape: 128 requests on one 8k context
+    (64, 8, 128, 13, 1000, False),
+    (32, 32, 128, 64, 1536, True),     # C2 shape (G = 1)
+    (32, 8, 128, 40, 700, False),
+    (8, 2, 64, 16, 64, True),          # C1 shape
+])
+@pytest.mark.parametrize("q_scale", [1.0, 4.0])
+def test_cascade_decode_vs_oracle(h_q, h_kv, hd, B, shared, contig, q_scale):
+    """rx_decode_cascade_append (shared prefix attended once on the tensor cores,
+    suffixes by the decode kernel, LSE merge) against the fp64 oracle; the KV
+    append (pool rows, req_to_token entries) is bit-identical to rx_decode_append."""
+    rng = np.random.default_rng(B * 31 + shared + hd)
+    suffix = [int(x) for x in rng.integers(1, 300, B)]          # >= 1: the new token is per-request
+    lens = [shared + s for s in suffix]
+    S = shared + sum(suffix) + 64
+    free = np.arange(1, S) if contig else rng.permutation(np.arange(1, S))
+    pre = free[:shared]
+    stride = max(lens) + 4
+    rtt = np.zeros((B, stride), dtype=np.int32)
+    new = np.zeros(B, dtype=np.int32)
+    off = shared
+    for b, L in enumerate(lens):
+        rtt[b, :shared] = pre
+        n_own = L - shared
+        rtt[b, shared:L - 1] = free[off:off + n_own - 1]
+        new[b] = free[off + n_own - 1]
+        off += n_own
+    kpool = _vals(rng, S, h_kv, KIND_K, hd)
+    vpool = _vals(rng, S, h_kv, KIND_V, hd)
+    q = _vals(rng, B, h_q, KIND_Q, hd, scale=q_scale).cuda()
+    kn = _vals(rng, B, h_kv, KIND_K, hd)
+    vn = _vals(rng, B, h_kv, KIND_V, hd)
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    seq = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    new_d = torch.from_numpy(new).cuda()
+    ws = torch.empty(rx.rx_decode_cascade_workspace_bytes(cfg, B, max(lens), shared) + 1, dtype=torch.uint8,
+                     device="cuda")
+    kp, vp, rtt_d = kpool.cuda(), vpool.cuda(), torch.from_numpy(rtt).cuda()
+    o = torch.full((B, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    rx.rx_decode_cascade_append(cfg, rtt_d, None, seq, max(lens), shared, q, kn.cuda(), vn.cuda(), new_d, kp, vp, o, ws)
+    # reference path for the append side effects
+    kp2, vp2, rtt2 = kpool.cuda(), vpool.cuda(), torch.from_numpy(rtt).cuda()
+    o2 = torch.empty_like(o)
+    ws2 = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, max(lens)) + 1, dtype=torch.uint8, device="cuda")
+    rx.rx_decode_append(cfg, rtt2, None, seq, max(lens), q, kn.cuda(), vn.cuda(), new_d, kp2, vp2, o2, ws2)
+    torch.cuda.synchronize()
+    assert torch.equal(kp, kp2) and torch.equal(vp, vp2) and torch.equal(rtt_d, rtt2)
+    pool = A.OraclePool(S, h_kv, hd)
+    pool.store(np.arange(S), kpool.float().numpy(), vpool.float().numpy())
+    pool.store(new, kn.float().numpy(), vn.float().numpy())
+    rows = [rtt[b].copy() for b in range(B)]
+    for b, L in enumerate(lens):
+        rows[b][L - 1] = new[b]
+    ref = A.decode(pool, rows, lens, q.float().cpu().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
+    _cmp(o, ref, f"cascade {h_q}/{h_kv}/{hd} B={B} shared={shared}")
+    assert (o.float() - o2.float()).abs().max().item() <= 2e-2
+
+
+def _decode_append_check(h_q, h_kv, hd, lens):
     """rx_decode_append == rx_store_kv + rtt append + rx_decode, bit for bit (pool, table, output)."""
     rng = np.random.default_rng(sum(lens))
     B = len(lens)
