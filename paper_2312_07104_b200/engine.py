@@ -100,7 +100,7 @@ class InputBank:
 
 class Engine:
     def __init__(self, wl, device="cuda", tp_rank=0, tp_size=1, plan_only=False, record=False,
-                 keep_outputs=False, gather=None):
+                 keep_outputs=False, gather=None, cascade=True):
         self.wl = wl
         self.shape = wl.shape
         self.device = device
@@ -124,6 +124,11 @@ class Engine:
         self.timer = None
         self._pin_cache = {}
         self.sink = None                     # callable(kind, o) invoked after every attention call
+        # shared-prefix (cascade) decode when the batch shares >= cascade_min_len cached slots
+        self.cascade = cascade
+        self.cascade_min_len = 256
+        self.cascade_min_batch = 4
+        self._shared = 0
         if not plan_only:
             hd = wl.shape.head_dim
             self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
@@ -245,6 +250,16 @@ class Engine:
             off += ext[b]
         self.stats["tree_s"] += time.perf_counter() - t0
         self._slots_host = slots
+        # cached prefix shared by every request of the batch (same radix path => same slots):
+        # decode steps attend it once for the whole batch (rx_decode_cascade_append)
+        mp = int(prefix.min())
+        if self.cascade and B >= self.cascade_min_batch and mp >= self.cascade_min_len:
+            diff = np.nonzero((slots[:, :mp] != slots[0:1, :mp]).any(axis=0))[0]
+            self._shared = int(diff[0]) if len(diff) else mp
+        else:
+            self._shared = 0
+        if self._shared < self.cascade_min_len:
+            self._shared = 0
         self._extend(rs, slots, prefix, ext)
         t0 = time.perf_counter()
         self._finish_many(rs, np.nonzero(n_out == 0)[0], slots)
@@ -366,12 +381,18 @@ class Engine:
         self._dec_used[i] = True
         max_seq = int(pos.max()) + 1
         o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
-        need = api.rx_decode_workspace_bytes(self.cfg, B, max_seq)
+        sh = self._shared
+        need = (api.rx_decode_cascade_workspace_bytes(self.cfg, B, max_seq, sh) if sh
+                else api.rx_decode_workspace_bytes(self.cfg, B, max_seq))
         if need > self._ws.numel():            # split count depends on (B, max_seq): grow on demand
             self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
         ev0 = self._tbeg()
-        api.rx_decode_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, q, k, v, d[:B], self.k_pool,
-                             self.v_pool, o, self._ws)
+        if sh:
+            api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, sh, q, k, v, d[:B],
+                                         self.k_pool, self.v_pool, o, self._ws)
+        else:
+            api.rx_decode_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, q, k, v, d[:B], self.k_pool,
+                                 self.v_pool, o, self._ws)
         nl = api.rx_last_launch_count()
         self.stats["launches"] += nl
         if ev0 is not None:

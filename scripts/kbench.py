@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--ext", type=int, default=512)
     ap.add_argument("--shared-prefix", action="store_true")
     ap.add_argument("--scatter", action="store_true", help="fragmented (non-contiguous) slots")
+    ap.add_argument("--cascade", type=int, default=0, help="decode: shared prefix length (cascade vs per-request)")
     ap.add_argument("--iters", type=int, default=20)
     a = ap.parse_args()
     h_q, h_kv, hd = a.h
@@ -49,7 +50,32 @@ def main():
         ts.sort()
         return ts[len(ts) // 2]
 
-    if a.kind == "decode":
+    if a.kind == "decode" and a.cascade:
+        # C5-style step: B requests share `cascade` cached tokens, each owns seq - cascade more
+        L, P = a.seq, a.cascade
+        S = P + B * (L - P) + 16
+        kp = torch.randn((S, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
+        vp = torch.randn_like(kp)
+        rtt = torch.zeros((B, L), dtype=torch.int32, device=dev)
+        rtt[:, :P] = torch.arange(1, P + 1, dtype=torch.int32, device=dev)
+        own = torch.arange(P + 1, P + 1 + B * (L - P), dtype=torch.int32, device=dev).view(B, L - P)
+        rtt[:, P:] = own
+        new = own[:, -1].contiguous()
+        q = torch.randn((B, h_q, hd), device=dev, generator=g).to(torch.bfloat16)
+        kn = torch.randn((B, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
+        vn = torch.randn_like(kn)
+        o = torch.empty_like(q)
+        lens = torch.full((B,), L, dtype=torch.int32, device=dev)
+        ws = torch.empty(max(rx.rx_decode_cascade_workspace_bytes(cfg, B, L, P),
+                             rx.rx_decode_workspace_bytes(cfg, B, L)) + 1, dtype=torch.uint8, device=dev)
+        ms_c = timeit(lambda: rx.rx_decode_cascade_append(cfg, rtt, None, lens, L, P, q, kn, vn, new, kp, vp, o, ws))
+        ms_p = timeit(lambda: rx.rx_decode_append(cfg, rtt, None, lens, L, q, kn, vn, new, kp, vp, o, ws))
+        uniq = (P + B * (L - P)) * h_kv * hd * 4
+        flops = 4 * hd * h_q * B * L
+        print(f"decode-step {h_q}/{h_kv}/{hd} B={B} L={L} shared={P}: cascade {ms_c*1e3:.1f} us "
+              f"({uniq/ms_c/1e6:.0f} GB/s unique, {flops/ms_c/1e9:.1f} TFLOP/s)  vs per-request {ms_p*1e3:.1f} us "
+              f"-> {ms_p/ms_c:.2f}x")
+    elif a.kind == "decode":
         L = a.seq
         S = (L if a.shared_prefix else B * L) + 16
         kp = torch.randn((S, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
