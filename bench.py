@@ -147,6 +147,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", default="C5", choices=["none", "C1", "C2", "C3", "C5"],
+                    help="also time this workload (reported under 'secondary', context only)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -317,6 +319,54 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
                "ms_per_step": e_ms / len(e2e_times)}
 
+    # ---------------------------------------------------------- secondary workload (context, same protocol)
+    secondary = None
+    if args.secondary != "none" and args.secondary != args.workload:
+        del bank, eng
+        torch.cuda.empty_cache()
+        wl2 = make_workload(args.secondary)
+        plan2, bank2 = plan_and_bank(wl2, dev, tp_rank=rank, tp_size=world)
+        eng2 = Engine(wl2, dev, tp_rank=rank, tp_size=world, gather=gather)
+        tok2 = plan2.stats["extend_tokens"] + plan2.stats["decode_tokens"]
+        for _ in range(args.warmup):
+            eng2.reset()
+            eng2.run_workload(bank2)
+        torch.cuda.synchronize()
+        eng2.enable_timing(True)
+        t2, kern2 = [], {}
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            eng2.timer = []
+            a.record()
+            eng2.reset()
+            eng2.run_workload(bank2)
+            b.record()
+            torch.cuda.synchronize()
+            barrier()
+            t2.append(a.elapsed_time(b))
+            for k_, v_ in eng2.timing_summary().items():
+                t = kern2.setdefault(k_, [0.0, 0, 0, 0.0])
+                for i in range(4):
+                    t[i] += v_[i]
+        ms2 = sum(t2)
+        if world > 1:
+            tt = torch.tensor([ms2], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms2 = float(tt.item())
+        secondary = {
+            "workload": wl2.name, "value": tok2 * len(t2) / (ms2 / 1000.0), "unit": "tokens/s",
+            "ms_per_step": ms2 / len(t2), "tokens_per_step": tok2,
+            "cache_hit_rate": plan2.stats["cached_prompt_tokens"] / max(1, plan2.stats["prompt_tokens"]),
+            "kernels": {k_: {"ms_per_step": v_[0] / len(t2), "calls_per_step": v_[2] // len(t2),
+                             ("tflops" if k_ == "extend" else "gbs_algorithmic"):
+                                 v_[3] / (v_[0] / 1000.0) / (1e12 if k_ == "extend" else 1e9)}
+                        for k_, v_ in kern2.items()},
+            "note": "context only; decode of a shared 8k prefix uses rx_decode_cascade_append"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, _ = run_oracle(args.workload)
@@ -335,7 +385,7 @@ def main():
                        "num_slots": wl.num_slots},
             "gpu_launches": launches, "roofline": roof, "kernels": kernels,
             "tree_ms_per_step": tree_s * 1000.0 / args.steps,
-            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "secondary": secondary,
         }
         print(json.dumps(line))
     if world > 1:

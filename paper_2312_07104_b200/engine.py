@@ -328,8 +328,9 @@ class Engine:
         ws_n = api.rx_decode_workspace_bytes(self.cfg, B, stride)
         self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
         # decode-step staging: a ring of RING pinned blocks [new_slots | seq_lens | rows]; the host never
-        # needs GPU results (tree ops + precomputed inputs), so it may run up to RING steps ahead
-        RING = 64
+        # needs GPU results (tree ops + precomputed inputs), so it may run up to RING steps ahead (a whole
+        # turn), hiding the next batch's host preparation behind the queued GPU work
+        RING = 1024                               # > the decode steps of any batch in C1-C5
         for i, used in enumerate(getattr(self, "_dec_used", [])):   # previous batch's copies out of the ring
             if used:
                 self._dec_ev[i].synchronize()
