@@ -34,6 +34,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "params.cuh"
 #include "ptx.cuh"
@@ -49,6 +50,19 @@ struct ExtendMaps {
 };
 
 constexpr int kExtThreads = 256;
+
+// Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
+// appends (code, item, clock) records; read back with rx_debug_ext_trace().
+__device__ unsigned long long rx_ext_trace[8192];
+__device__ unsigned int rx_ext_trace_n;
+__device__ __forceinline__ void ext_trace(int on, int code, int item) {
+  if (on && blockIdx.x == 0) {
+    const unsigned int i = atomicAdd(&rx_ext_trace_n, 1u);
+    if (i < 8192)
+      rx_ext_trace[i] = (static_cast<unsigned long long>(code) << 56) |
+                        (static_cast<unsigned long long>(item & 0xFFFFFF) << 32) | static_cast<unsigned int>(clock());
+  }
+}
 constexpr int kBN = 128;          // kv tokens per tile
 constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
 
@@ -198,6 +212,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(q_full + qb, C::Q_BYTES);
+          ext_trace(p.trace, 1, it);
 #pragma unroll
           for (int c = 0; c < C::NCB; ++c)
             tma_load_3d(sq + qb * C::Q_BYTES + c * 128 * kTileRowBytes, &maps.q, q_full + qb, c * 64, I.g * G,
@@ -207,6 +222,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       for (int j = 0; j < I.n_tiles; ++j, ++jg) {
         const int st = jg % NS, rnd = jg / NS;
         mbar_wait(empty + st, (rnd & 1) ^ 1);
+        if (lane == 0) ext_trace(p.trace, is_v ? 3 : 2, jg);
         const uint32_t d = base_s + st * C::KV_BYTES;
         // prefix tile: one 3-D TMA box when its 128 slots are consecutive, else a
         // cp.async gather (see below); new-KV tile: one 3-D TMA box
@@ -294,6 +310,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
                     umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
           }
           tc_commit(s_full + (g_ & 1));
+          ext_trace(p.trace, 4, g_);
           tc_commit(k_empty + st);                          // K_g is free once S_g retires
           if (j == I.n_tiles - 1) tc_commit(q_empty + qb);  // last read of this Q buffer issued
         };
@@ -302,6 +319,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           if (j + 1 < I.n_tiles) issue_s(j + 1);
           const int g_ = jg + j;
           mbar_wait(p_full + (g_ & 1), (g_ >> 1) & 1);
+          ext_trace(p.trace, 5, g_);
           tc_fence_after();
           const int st = g_ % C::VS;
           mbar_wait(v_full + st, (g_ / C::VS) & 1);
@@ -314,6 +332,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
                     (j > 0 || k > 0) ? 1u : 0u);
           tc_commit(v_empty + st);
           tc_commit(o_done);
+          ext_trace(p.trace, 6, g_);
         }
         tc_commit(o_ready + qb);
         jg += I.n_tiles;
@@ -336,6 +355,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         const int g_ = jg + j;
         const uint32_t t_s = tmem + lane_off + (g_ & 1) * 128;
         mbar_wait(s_full + (g_ & 1), (g_ >> 1) & 1);
+        if (threadIdx.x == 128) ext_trace(p.trace, 7, g_);
         tc_fence_after();
         float sv[kBN];
 #pragma unroll
@@ -412,9 +432,11 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full + (g_ & 1));
+        if (threadIdx.x == 128) ext_trace(p.trace, 8, g_);
       }
       // epilogue: O[qb] complete once this item's last P.V landed
       mbar_wait(o_ready + qb, (it >> 1) & 1);
+      if (threadIdx.x == 128) ext_trace(p.trace, 9, it);
       tc_fence_after();
       const uint32_t t_o = tmem + lane_off + C::O_COL + qb * HD;
       const float inv = 1.f / l;
@@ -449,6 +471,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(o_free + qb);
+      if (threadIdx.x == 128) ext_trace(p.trace, 10, it);
       jg += I.n_tiles;
       ++it;
     }
@@ -534,6 +557,9 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   }
   ExtendParams pp = p;
   pp.batch = batch;
+  static int trace_env = -1;
+  if (trace_env < 0) trace_env = getenv("RX_EXT_TRACE") ? 1 : 0;
+  pp.trace = trace_env;
   pp.max_qtiles = (max_ext + TOK - 1) / TOK;
   const int64_t items = int64_t(pp.max_qtiles) * p.h_kv * (p.cascade ? p.n_kv_splits : batch);
   static int sms = 0;
@@ -570,3 +596,16 @@ cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void
 }
 
 }  // namespace rx
+
+// Development only (not part of include/rx.h): copy and reset the extend-kernel
+// timeline written when RX_EXT_TRACE is set.  Returns the record count.
+extern "C" int rx_debug_ext_trace(unsigned long long* out, int cap) {
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, rx::rx_ext_trace_n, sizeof(n));
+  if (n > 8192) n = 8192;
+  if (out && cap > 0) cudaMemcpyFromSymbol(out, rx::rx_ext_trace, sizeof(unsigned long long) * (n < unsigned(cap) ? n : cap));
+  unsigned int z = 0;
+  cudaMemcpyToSymbol(rx::rx_ext_trace_n, &z, sizeof(z));
+  return int(n);
+}

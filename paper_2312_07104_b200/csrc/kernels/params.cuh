@@ -70,6 +70,7 @@ struct ExtendParams {
   int part_splits;
   int part_base;
   int cas_prefix;               // shared prefix length (cascade mode; prefix_lens unused)
+  int trace;                    // development timeline tracer (RX_EXT_TRACE)
 };
 
 struct DecodePlan {

@@ -265,21 +265,30 @@ class Engine:
         self._finish_many(rs, np.nonzero(n_out == 0)[0], slots)
         running = np.nonzero(n_out > 0)[0]
         self.stats["tree_s"] += time.perf_counter() - t0
+        # Decode phase, in two passes.  (A) every tree op of the phase — one slot per running request
+        # per step (R23), finished requests' dec_ref + insert — runs on the host first: none of it
+        # depends on GPU results (the mock-model tokens are known).  (B) the phase's per-step
+        # metadata goes to the device in ONE copy and the decode kernels are launched back to back.
         step = 0
+        steps = []
         while len(running):
             t0 = time.perf_counter()
             new = self._alloc(len(running))
             pos = n_prompt[running] + step
             slots[running, pos] = new
-            self.stats["tree_s"] += time.perf_counter() - t0
-            self._decode(rs, running, new, pos)
+            steps.append((running, new, pos))
+            self.stats["decode_tokens"] += len(running)
+            if self.plan_only:
+                hs = np.array([rs[b].hashes[p_] for b, p_ in zip(running, pos)], dtype=np.uint64)
+                self.calls.append(CallPlan("decode", hs, {"B": len(running)}))
             step += 1
-            t0 = time.perf_counter()
             done = n_out[running] <= step
             if done.any():
                 self._finish_many(rs, running[done], slots)
             running = running[~done]
             self.stats["tree_s"] += time.perf_counter() - t0
+        if steps and not self.plan_only:
+            self._decode_phase(steps)
         self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
         return rs
 
@@ -327,18 +336,6 @@ class Engine:
         self._B = B
         ws_n = api.rx_decode_workspace_bytes(self.cfg, B, stride)
         self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
-        # decode-step staging: a ring of RING pinned blocks [new_slots | seq_lens | rows]; the host never
-        # needs GPU results (tree ops + precomputed inputs), so it may run up to RING steps ahead (a whole
-        # turn), hiding the next batch's host preparation behind the queued GPU work
-        RING = 1024                               # > the decode steps of any batch in C1-C5
-        for i, used in enumerate(getattr(self, "_dec_used", [])):   # previous batch's copies out of the ring
-            if used:
-                self._dec_ev[i].synchronize()
-        self._dec_pin = self._pinned("dec", RING * 3 * B).view(RING, 3 * B)
-        self._dec_dev = torch.empty((RING, 3 * B), dtype=torch.int32, device=dev)
-        self._dec_ev = [torch.cuda.Event() for _ in range(RING)]
-        self._dec_used = [False] * RING
-        self._dec_n = 0
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         ev0 = self._tbeg()
         api.rx_extend(self.cfg, self._rtt, None, dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
@@ -357,55 +354,54 @@ class Engine:
         if self.keep_outputs:
             self.outputs.append(("extend", o, {"ext": ext.tolist()}))
 
-    def _decode(self, rs, running, new_slots, pos):
-        B = len(running)
-        self.stats["decode_tokens"] += B
-        if self.plan_only:
-            hs = np.array([rs[b].hashes[p] for b, p in zip(running, pos)], dtype=np.uint64)
-            self.calls.append(CallPlan("decode", hs, {"B": B}))
-            return
+    def _decode_phase(self, steps):
+        """Launch a batch's decode steps: one H2D of [new_slots | seq_lens | rows] for every step,
+        then one rx_decode_append (or rx_decode_cascade_append) per step."""
         dev = self.device
-        q, k, v = self.bank.dec[self._dec_i]
-        self._dec_i += 1
-        i = self._dec_n % len(self._dec_ev)
-        self._dec_n += 1
-        if self._dec_used[i]:
-            self._dec_ev[i].synchronize()           # the H2D copy from RING steps ago consumed this block
-        pin = self._dec_pin[i]
-        pn = pin.numpy()
-        pn[0:B] = new_slots
-        pn[B:2 * B] = pos + 1                       # seq_len counts the new token
-        pn[2 * B:3 * B] = running                   # table row of each running request
-        d = self._dec_dev[i, :3 * B]
-        d.copy_(pin[:3 * B], non_blocking=True)
-        self._dec_ev[i].record()
-        self._dec_used[i] = True
-        max_seq = int(pos.max()) + 1
-        o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+        offs = np.zeros(len(steps) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([3 * len(r) for r, _, _ in steps])
+        stage = self._pinned("dec", int(offs[-1]))
+        sn = stage.numpy()
+        need = 0
         sh = self._shared
-        need = (api.rx_decode_cascade_workspace_bytes(self.cfg, B, max_seq, sh) if sh
-                else api.rx_decode_workspace_bytes(self.cfg, B, max_seq))
-        if need > self._ws.numel():            # split count depends on (B, max_seq): grow on demand
+        for (running, new, pos), o0 in zip(steps, offs):
+            B = len(running)
+            sn[o0:o0 + B] = new
+            sn[o0 + B:o0 + 2 * B] = pos + 1             # seq_len counts the new token
+            sn[o0 + 2 * B:o0 + 3 * B] = running         # table row of each running request
+            ms = int(pos.max()) + 1
+            need = max(need, api.rx_decode_cascade_workspace_bytes(self.cfg, B, ms, sh) if sh
+                       else api.rx_decode_workspace_bytes(self.cfg, B, ms))
+        d_all = stage.to(dev, non_blocking=True)
+        self._pinned_done("dec")
+        if need > self._ws.numel():
             self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
-        ev0 = self._tbeg()
-        if sh:
-            api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, sh, q, k, v, d[:B],
-                                         self.k_pool, self.v_pool, o, self._ws)
-        else:
-            api.rx_decode_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, q, k, v, d[:B], self.k_pool,
-                                 self.v_pool, o, self._ws)
-        nl = api.rx_last_launch_count()
-        self.stats["launches"] += nl
-        if ev0 is not None:
-            # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot indices,
-            # computed after the timed region from (slots, running, pos)
-            self._tend(ev0, "decode", (self._slots_host, running.copy(), pos.copy()), nl)
-        if self.gather is not None:
-            o = self.gather(o)
-        if self.sink is not None:
-            self.sink("decode", o)
-        if self.keep_outputs:
-            self.outputs.append(("decode", o, {"B": B}))
+        for (running, new, pos), o0 in zip(steps, offs):
+            B = len(running)
+            q, k, v = self.bank.dec[self._dec_i]
+            self._dec_i += 1
+            d = d_all[o0:o0 + 3 * B]
+            max_seq = int(pos.max()) + 1
+            o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+            ev0 = self._tbeg()
+            if sh:
+                api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, sh, q, k, v,
+                                             d[:B], self.k_pool, self.v_pool, o, self._ws)
+            else:
+                api.rx_decode_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, q, k, v, d[:B],
+                                     self.k_pool, self.v_pool, o, self._ws)
+            nl = api.rx_last_launch_count()
+            self.stats["launches"] += nl
+            if ev0 is not None:
+                # algorithmic bytes (SURVEY §8(d)): distinct pool rows read (K+V) + q + o + slot indices,
+                # computed after the timed region from (slots, running, pos)
+                self._tend(ev0, "decode", (self._slots_host, running, pos), nl)
+            if self.gather is not None:
+                o = self.gather(o)
+            if self.sink is not None:
+                self.sink("decode", o)
+            if self.keep_outputs:
+                self.outputs.append(("decode", o, {"B": B}))
 
     # ------------------------------------------------------------------ pinned staging
     def _pinned(self, name, n):
