@@ -121,6 +121,16 @@ typedef void (*rx_evict_cb)(void* user, const int32_t* slots, int64_t n);
  * cb may be null. */
 rx_status rx_evict(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb, void* user);
 
+/* rx_evict with the evicted leaf's token PATH: cb(user, path, path_len,
+ * leaf_start, slots, n) where path[0..path_len) are the tokens from the root
+ * to the end of the evicted leaf and the leaf owned path[leaf_start..path_len)
+ * (n = path_len - leaf_start slots).  Same eviction order and effects as
+ * rx_evict.  This is what a data-parallel worker reports to the router's
+ * eviction queue (App. A.4). */
+typedef void (*rx_evict_path_cb)(void* user, const int32_t* path, int64_t path_len, int64_t leaf_start,
+                                 const int32_t* slots, int64_t n);
+rx_status rx_evict_paths(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_path_cb cb, void* user);
+
 /* Token-slot pool.  rx_alloc returns the n smallest free slots in ascending
  * order into out[0..n) (R8), or RX_E_NOMEM with no side effect.
  * rx_free returns slots to the pool (RX_E_INVALID on a slot out of range or
@@ -170,6 +180,43 @@ int64_t rx_clock(const rx_cache* c);
  * Writes at most cap bytes (NUL-terminated) into buf and returns the full
  * length (excluding NUL); call with cap = 0 to size the buffer. */
 int64_t rx_dump_json(const rx_cache* c, char* buf, int64_t cap);
+
+/* ----------------------------------------------------------------------- */
+/*  Data-parallel router (App. A.4)          */
+/* ----------------------------------------------------------------------- */
+/* "each worker maintains its own sub-tree, while the router oversees a
+ * meta-tree ... a trie that tracks all sub-trees and their associated
+ * devices"; dispatch by affinity (shared-prefix length with a worker and
+ * with other requests of the batch); worker evictions are committed to a queue
+ * that the router applies later (weakly consistent: a stale entry costs a cold
+ * dispatch, never a wrong result).  Up to 64 workers.  Host only.
+ * Reading R24: affinity[w] = tokens of the request matched along
+ * the meta-tree while w is in every edge's worker set from the root;
+ * score[w] = affinity[w] - load_weight * loads[w]; argmax, ties -> smaller
+ * load -> smaller id; the chosen worker is credited with the request's tokens
+ * immediately (so later requests of the batch sharing them follow it) and
+ * loads[w] += tokens not already cached there. */
+typedef struct rx_router rx_router;
+rx_status rx_router_create(int32_t num_workers, rx_router** out);
+void rx_router_destroy(rx_router* r);
+/* aff: int64 [num_workers] */
+rx_status rx_router_affinity(const rx_router* r, const int32_t* tokens, int64_t n, int64_t* aff);
+/* Requests b = 0..batch-1 are tokens[offsets[b] .. offsets[b+1]); loads
+ * (int64 [num_workers], in/out) is each worker's outstanding work in tokens;
+ * worker_out[b] receives the assignment, affinity_out[b] (nullable) its
+ * affinity.  Processes requests in order. */
+rx_status rx_router_dispatch(rx_router* r, int32_t batch, const int32_t* tokens, const int64_t* offsets,
+                             int64_t* loads, double load_weight, int32_t* worker_out, int64_t* affinity_out);
+/* worker cached tokens[0..n) (e.g. after rx_insert on that worker) */
+rx_status rx_router_insert(rx_router* r, int32_t worker, const int32_t* tokens, int64_t n);
+/* worker evicted the leaf path[leaf_start..path_len) (rx_evict_paths callback) */
+rx_status rx_router_queue_evict(rx_router* r, int32_t worker, const int32_t* path, int64_t path_len,
+                                int64_t leaf_start);
+/* apply the queued evictions in FIFO order; returns how many were applied */
+int64_t rx_router_sync(rx_router* r);
+int64_t rx_router_queue_len(const rx_router* r);
+/* deterministic pre-order JSON {"tokens","mask","children"} (same contract as rx_dump_json) */
+int64_t rx_router_dump_json(const rx_router* r, char* buf, int64_t cap);
 
 /* ======================================================================= */
 /*  2. Attention over the token-slot KV pool (device, sm_100a)              */

@@ -27,6 +27,7 @@ class AttnCfg(C.Structure):
 
 
 EVICT_CB = C.CFUNCTYPE(None, vp, P32, i64)
+EVICT_PATH_CB = C.CFUNCTYPE(None, vp, P32, i64, i64, P32, i64)
 
 # symbol -> (restype, argtypes); the set of names is exactly include/rx.h's declarations
 SIGNATURES = {
@@ -42,6 +43,16 @@ SIGNATURES = {
     "rx_alloc": (C.c_int, [vp, i64, P32]),
     "rx_free": (C.c_int, [vp, P32, i64]),
     "rx_alloc_evict": (C.c_int, [vp, i64, P32, P64, EVICT_CB, vp]),
+    "rx_evict_paths": (C.c_int, [vp, i64, P64, EVICT_PATH_CB, vp]),
+    "rx_router_create": (C.c_int, [i32, C.POINTER(vp)]),
+    "rx_router_destroy": (None, [vp]),
+    "rx_router_affinity": (C.c_int, [vp, P32, i64, P64]),
+    "rx_router_dispatch": (C.c_int, [vp, i32, P32, P64, P64, C.c_double, P32, P64]),
+    "rx_router_insert": (C.c_int, [vp, i32, P32, i64]),
+    "rx_router_queue_evict": (C.c_int, [vp, i32, P32, i64, i64]),
+    "rx_router_sync": (i64, [vp]),
+    "rx_router_queue_len": (i64, [vp]),
+    "rx_router_dump_json": (i64, [vp, C.c_char_p, i64]),
     "rx_match_prefix_batch": (C.c_int, [vp, i32, P32, P64, P64, P64, P32]),
     "rx_inc_ref_batch": (C.c_int, [vp, i32, P64, P64]),
     "rx_finish_batch": (C.c_int, [vp, i32, P64, P32, P64, P32, P64, P64, P64]),

@@ -13,7 +13,7 @@ import json
 
 import numpy as np
 
-from ._lib import lib, AttnCfg, EVICT_CB, RxError, P32, P64
+from ._lib import lib, AttnCfg, EVICT_CB, EVICT_PATH_CB, RxError, P32, P64
 
 _I32 = np.int32
 
@@ -92,6 +92,19 @@ class RadixCache:
         _check(lib.rx_evict(self._h, needed, C.byref(ev), self._cb, None), "rx_evict")
         return ev.value, self._runs
 
+    def rx_evict_paths(self, needed: int):
+        """-> (evicted, [(path tokens, leaf_start, slots)] in eviction order)"""
+        out = []
+
+        def cb(user, path, plen, leaf_start, slots, n):
+            out.append((np.ctypeslib.as_array(path, shape=(plen,)).copy(), int(leaf_start),
+                        np.ctypeslib.as_array(slots, shape=(n,)).copy() if n else np.zeros(0, _I32)))
+
+        f = EVICT_PATH_CB(cb)
+        ev = C.c_int64()
+        _check(lib.rx_evict_paths(self._h, needed, C.byref(ev), f, None), "rx_evict_paths")
+        return ev.value, out
+
     def rx_alloc(self, n: int):
         """n smallest free slots (ascending) or None on RX_E_NOMEM."""
         out = np.empty(max(n, 1), dtype=_I32)
@@ -164,6 +177,68 @@ class RadixCache:
         n = lib.rx_dump_json(self._h, None, 0)
         buf = C.create_string_buffer(n + 1)
         lib.rx_dump_json(self._h, buf, n + 1)
+        return json.loads(buf.value.decode())
+
+
+class Router:
+    """rx_router: the data-parallel meta-tree router (App. A.4)."""
+
+    def __init__(self, num_workers: int):
+        h = C.c_void_p()
+        _check(lib.rx_router_create(num_workers, C.byref(h)), "rx_router_create")
+        self._h = h
+        self.num_workers = num_workers
+
+    def close(self):
+        if self._h:
+            lib.rx_router_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rx_router_affinity(self, tokens):
+        t = _i32(tokens)
+        aff = np.empty(self.num_workers, dtype=np.int64)
+        _check(lib.rx_router_affinity(self._h, _p32(t), len(t), aff.ctypes.data_as(P64)), "rx_router_affinity")
+        return aff
+
+    def rx_router_dispatch(self, requests, loads, load_weight: float):
+        """requests: list of token arrays; loads: int64 [W] (updated in place) -> (workers, affinities)"""
+        t = _i32(np.concatenate([np.asarray(r, dtype=np.int32) for r in requests]) if len(requests)
+                 else np.zeros(0, np.int32))
+        off = np.zeros(len(requests) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([len(r) for r in requests])
+        if not isinstance(loads, np.ndarray) or loads.dtype != np.int64 or not loads.flags.c_contiguous:
+            raise ValueError("loads must be a contiguous int64 numpy array (updated in place)")
+        w = np.empty(len(requests), dtype=_I32)
+        a = np.empty(len(requests), dtype=np.int64)
+        _check(lib.rx_router_dispatch(self._h, len(requests), _p32(t), off.ctypes.data_as(P64),
+                                      loads.ctypes.data_as(P64), float(load_weight), _p32(w), a.ctypes.data_as(P64)),
+               "rx_router_dispatch")
+        return w, a
+
+    def rx_router_insert(self, worker: int, tokens):
+        t = _i32(tokens)
+        _check(lib.rx_router_insert(self._h, worker, _p32(t), len(t)), "rx_router_insert")
+
+    def rx_router_queue_evict(self, worker: int, path, leaf_start: int):
+        t = _i32(path)
+        _check(lib.rx_router_queue_evict(self._h, worker, _p32(t), len(t), leaf_start), "rx_router_queue_evict")
+
+    def rx_router_sync(self) -> int:
+        return lib.rx_router_sync(self._h)
+
+    def rx_router_queue_len(self) -> int:
+        return lib.rx_router_queue_len(self._h)
+
+    def rx_router_dump_json(self) -> dict:
+        n = lib.rx_router_dump_json(self._h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib.rx_router_dump_json(self._h, buf, n + 1)
         return json.loads(buf.value.decode())
 
 

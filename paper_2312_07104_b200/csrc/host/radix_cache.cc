@@ -295,7 +295,8 @@ rx_status rx_dec_ref(rx_cache* c, rx_node h, int64_t* d_evictable) {
   return RX_OK;
 }
 
-rx_status rx_evict(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb, void* user) {
+static rx_status evict_impl(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb, rx_evict_path_cb pcb,
+                            void* user) {
   if (!c || !evicted) return RX_E_INVALID;
   *evicted = 0;
   if (needed <= 0) return RX_OK;
@@ -323,6 +324,16 @@ rx_status rx_evict(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb
     int64_t len = int64_t(n->tokens.size());
     c->release(n->slots.data(), len);
     if (cb) cb(user, n->slots.data(), len);
+    if (pcb) {
+      std::vector<const Node*> chain;                 // root-exclusive path p ... n
+      for (const Node* a = p; a != &c->root; a = a->parent) chain.push_back(a);
+      std::vector<int32_t> path;
+      for (auto it = chain.rbegin(); it != chain.rend(); ++it)
+        path.insert(path.end(), (*it)->tokens.begin(), (*it)->tokens.end());
+      const int64_t leaf_start = int64_t(path.size());
+      path.insert(path.end(), n->tokens.begin(), n->tokens.end());
+      pcb(user, path.data(), int64_t(path.size()), leaf_start, n->slots.data(), len);
+    }
     got += len;
     c->evictable -= len;
     c->cached -= len;
@@ -332,6 +343,14 @@ rx_status rx_evict(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb
   }
   *evicted = got;
   return RX_OK;
+}
+
+rx_status rx_evict(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_cb cb, void* user) {
+  return evict_impl(c, needed, evicted, cb, nullptr, user);
+}
+
+rx_status rx_evict_paths(rx_cache* c, int64_t needed, int64_t* evicted, rx_evict_path_cb cb, void* user) {
+  return evict_impl(c, needed, evicted, nullptr, cb, user);
 }
 
 rx_status rx_alloc(rx_cache* c, int64_t n, int32_t* out) {
