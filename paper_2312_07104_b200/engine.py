@@ -124,6 +124,7 @@ class Engine:
         self.timer = None
         self._pin_cache = {}
         self.sink = None                     # callable(kind, o) invoked after every attention call
+        self.evict_listener = None           # callable(path tokens, leaf_start) per evicted leaf (DP workers)
         # shared-prefix (cascade) decode when the batch shares >= cascade_min_len cached slots
         self.cascade = cascade
         self.cascade_min_len = 256
@@ -144,7 +145,14 @@ class Engine:
         s = c.rx_alloc(n)
         if s is None:
             short = n - c.rx_available()
-            ev, runs = c.rx_evict(short)
+            if self.evict_listener is not None:
+                # data-parallel worker: report evicted token paths to the router's queue (App. A.4)
+                ev, paths = c.rx_evict_paths(short)
+                runs = [sl for _, _, sl in paths]
+                for path, leaf_start, _ in paths:
+                    self.evict_listener(path, leaf_start)
+            else:
+                ev, runs = c.rx_evict(short)
             self._rec("evict", short, ev, tuple(tuple(int(x) for x in r) for r in runs))
             s = c.rx_alloc(n)
             if s is None:
