@@ -15,7 +15,10 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python paper_2312_07104_b200/build.py` "
                       "(or __graft_entry__.build()); there is no CPU fallback")
 
-lib = C.CDLL(LIB_PATH)
+# RX_LIB_OVERRIDE: load a sanitizer build of the HOST half instead (scripts/asan_host.sh);
+# device entry points are then absent and only the tree/router tests may run.
+_override = os.environ.get("RX_LIB_OVERRIDE")
+lib = C.CDLL(_override if _override else LIB_PATH)
 
 i32, i64, f32, vp, sz = C.c_int32, C.c_int64, C.c_float, C.c_void_p, C.c_size_t
 P32 = C.POINTER(C.c_int32)
@@ -77,6 +80,8 @@ SIGNATURES = {
 }
 
 for _name, (_res, _args) in SIGNATURES.items():
+    if _override and not hasattr(lib, _name):
+        continue
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args
