@@ -51,20 +51,15 @@ struct ExtendMaps {
 
 constexpr int kExtThreads = 256;
 
-// Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
-// appends (code, item, clock) records; read back with rx_debug_ext_trace().
-__device__ unsigned long long rx_ext_trace[8192];
-__device__ unsigned int rx_ext_trace_n;
-__device__ __forceinline__ void ext_trace(int on, int code, int item) {
-  if (on && blockIdx.x == 0) {
-    const unsigned int i = atomicAdd(&rx_ext_trace_n, 1u);
-    if (i < 8192)
-      rx_ext_trace[i] = (static_cast<unsigned long long>(code) << 56) |
-                        (static_cast<unsigned long long>(item & 0xFFFFFF) << 32) | static_cast<unsigned int>(clock());
-  }
-}
-constexpr int kBN = 128;          // kv tokens per tile
+constexpr int kBN = 128;            // kv tokens per tile
 constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
+
+// Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
+// stores clock64 per (event code, item/tile index); read back with rx_debug_ext_trace().
+__device__ unsigned long long rx_ext_trace[16 * 1024];   // [code][item & 1023]: clock64, CTA 0 only
+__device__ __forceinline__ void ext_trace(int on, int code, int item) {
+  if (on && blockIdx.x == 0) rx_ext_trace[code * 1024 + (item & 1023)] = clock64();   // plain store, no wait
+}
 
 template <int HD>
 struct ExtCfg {
@@ -77,7 +72,7 @@ struct ExtCfg {
   static constexpr int KS = HD == 128 ? 3 : 4;
   static constexpr int VS = HD == 128 ? 2 : 3;
   static constexpr int SMEM_DATA = 2 * Q_BYTES + (KS + VS) * KV_BYTES;
-  static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 1024 /*barriers + item ring*/;
   static constexpr uint32_t TMEM_COLS = 512;                  // S0 | S1 | O0 | O1
   static constexpr uint32_t O_COL = 256;                      // O buffer b at O_COL + b*HD
 };
@@ -90,6 +85,32 @@ struct ExtItem {
   int split;            // cascade chunk index
   const int32_t* slots;
 };
+
+// Item ring: warp 2 resolves the CTA's work items (32 candidates per round, one
+// per lane, so the request-array loads overlap) and publishes descriptors in
+// shared memory; the 7 consumers (K producer, MMA, V producer, 4 softmax warps)
+// read them instead of each walking the list with dependent global loads.
+constexpr int kRing = 8;
+constexpr int kRingConsumers = 7;
+
+struct RingCursor {
+  int slot = 0;
+  uint32_t phase = 0;
+};
+
+// all lanes of the calling warp (or the lone MMA lane) read the descriptor;
+// `arrive` marks the lane that releases the slot
+__device__ __forceinline__ bool ring_pop(ExtItem& I, RingCursor& c, const ExtItem* ring, uint64_t* full,
+                                         uint64_t* empty, bool arrive) {
+  mbar_wait(full + c.slot, c.phase);
+  I = ring[c.slot];
+  if (arrive) mbar_arrive(empty + c.slot);
+  if (++c.slot == kRing) {
+    c.slot = 0;
+    c.phase ^= 1;
+  }
+  return I.b >= 0;
+}
 
 template <int TOK>
 __device__ __forceinline__ bool ext_item(const ExtendParams& p, int qt, int w, ExtItem& it) {
@@ -156,7 +177,10 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   uint64_t* o_done = p_full + 2;                      // one phase per P.V
   uint64_t* o_ready = o_done + 1;                     // [2] one phase per item (its last P.V)
   uint64_t* o_free = o_ready + 2;                     // [2] epilogue has read O[b]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* desc_full = o_free + 2;                   // [kRing] item descriptors published
+  uint64_t* desc_empty = desc_full + kRing;           // [kRing] ... and consumed by all 7 roles
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(desc_empty + kRing);
+  ExtItem* ring = reinterpret_cast<ExtItem*>(smem + C::SMEM_DATA + 512);
 
   const int qt = p.max_qtiles;
   const int W = p.cascade ? qt * p.h_kv * p.n_kv_splits : qt * p.h_kv * p.batch;
@@ -180,6 +204,10 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(v_empty + s, 1);
     }
     mbar_init(o_done, 1);
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(desc_full + i, 1);
+      mbar_init(desc_empty + i, kRingConsumers);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -205,8 +233,8 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     }
     int it = 0, jg = 0;
     ExtItem I;
-    for (int w = blockIdx.x; w < W; w += gridDim.x) {
-      if (!ext_item<TOK>(p, qt, w, I)) continue;
+    RingCursor rc;
+    while (ring_pop(I, rc, ring, desc_full, desc_empty, lane == 0)) {
       if (!is_v) {
         const int qb = it & 1;
         if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
@@ -288,8 +316,8 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
       int it = 0, jg = 0;
       ExtItem I;
-      for (int w = blockIdx.x; w < W; w += gridDim.x) {
-        if (!ext_item<TOK>(p, qt, w, I)) continue;
+      RingCursor rc;
+      while (ring_pop(I, rc, ring, desc_full, desc_empty, true)) {
         const int qb = it & 1;
         const uint32_t qa = sq + qb * C::Q_BYTES;
         const uint32_t t_o = tmem + C::O_COL + qb * HD;
@@ -346,8 +374,8 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
     int it = 0, jg = 0;
     ExtItem I;
-    for (int w = blockIdx.x; w < W; w += gridDim.x) {
-      if (!ext_item<TOK>(p, qt, w, I)) continue;
+    RingCursor rc;
+    while (ring_pop(I, rc, ring, desc_full, desc_empty, lane == 0)) {
       const int qb = it & 1;
       const int rel = I.t * TOK + i_tok;           // position relative to prefix_len
       float m_ref = -INFINITY, l = 0.f;
@@ -475,10 +503,41 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       jg += I.n_tiles;
       ++it;
     }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ item scheduler (+ TMEM owner)
+    // (A5, storing the new K/V rows into their slots, is extend_store_kernel,
+    // launched just before this kernel on the same stream.)
+    RingCursor c;
+    const int stride = 32 * gridDim.x;
+    for (int base = blockIdx.x; base < W; base += stride) {
+      const int w = base + lane * gridDim.x;
+      ExtItem I;
+      const bool v = w < W && ext_item<TOK>(p, qt, w, I);
+      unsigned m = __ballot_sync(0xffffffffu, v);
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        mbar_wait(desc_empty + c.slot, c.phase ^ 1);
+        if (lane == l) {
+          ring[c.slot] = I;
+          mbar_arrive(desc_full + c.slot);
+        }
+        __syncwarp();
+        if (++c.slot == kRing) {
+          c.slot = 0;
+          c.phase ^= 1;
+        }
+      }
+    }
+    mbar_wait(desc_empty + c.slot, c.phase ^ 1);      // sentinel
+    if (lane == 0) {
+      ExtItem I{};
+      I.b = -1;
+      ring[c.slot] = I;
+      mbar_arrive(desc_full + c.slot);
+    }
+    __syncwarp();
   }
-  // warp 2 only owns the TMEM allocation.  (A5, storing the new K/V rows into
-  // their slots, is extend_store_kernel, launched just before this kernel on
-  // the same stream: this kernel reads new K/V from k_new / v_new directly.)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -597,15 +656,14 @@ cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void
 
 }  // namespace rx
 
-// Development only (not part of include/rx.h): copy and reset the extend-kernel
-// timeline written when RX_EXT_TRACE is set.  Returns the record count.
+// Development only (not part of include/rx.h): copy and clear the extend-kernel
+// timeline ([16 codes][1024 items] clock64 values, 0 = not recorded) written
+// when RX_EXT_TRACE is set.  Returns the number of values copied.
 extern "C" int rx_debug_ext_trace(unsigned long long* out, int cap) {
-  unsigned int n = 0;
+  const int n = 16 * 1024;
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(&n, rx::rx_ext_trace_n, sizeof(n));
-  if (n > 8192) n = 8192;
-  if (out && cap > 0) cudaMemcpyFromSymbol(out, rx::rx_ext_trace, sizeof(unsigned long long) * (n < unsigned(cap) ? n : cap));
-  unsigned int z = 0;
-  cudaMemcpyToSymbol(rx::rx_ext_trace_n, &z, sizeof(z));
-  return int(n);
+  if (out && cap > 0) cudaMemcpyFromSymbol(out, rx::rx_ext_trace, sizeof(unsigned long long) * (n < cap ? n : cap));
+  static unsigned long long zero[16 * 1024];
+  cudaMemcpyToSymbol(rx::rx_ext_trace, zero, sizeof(zero));
+  return n < cap ? n : cap;
 }

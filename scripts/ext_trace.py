@@ -52,26 +52,25 @@ def main():
         torch.cuda.synchronize()
         f(None, 0)
     rx.rx_extend(cfg, rtt, None, pre, ext, ind, N, E, P, q, kn, vn, kp, vp, o)
-    buf = (C.c_ulonglong * 8192)()
-    n = f(buf, 8192)
-    recs = np.frombuffer(buf, dtype=np.uint64)[:n]
-    code = (recs >> np.uint64(56)).astype(int)
-    item = ((recs >> np.uint64(32)) & np.uint64(0xFFFFFF)).astype(int)
-    clk = (recs & np.uint64(0xFFFFFFFF)).astype(np.int64)
-    clk = (clk - clk.min()) % (1 << 32)
-    order = np.argsort(clk, kind="stable")
-    print(f"{n} records; span {clk.max()} cycles")
-    last = {}
-    for i in order[:400]:
-        c, it, t = code[i], item[i], clk[i]
-        dt = t - last.get(c, t)
-        last[c] = t
-        print(f"{t:10d}  {NAMES.get(c, c):6s} #{it:<5d} (+{dt} since prev {NAMES.get(c, c)})")
-    # per-code average interval
-    for c in sorted(set(code)):
-        ts = np.sort(clk[code == c])
-        if len(ts) > 2:
-            print(f"{NAMES.get(c, c):6s}: {len(ts)} events, mean interval {np.diff(ts).mean():.0f} cycles")
+    buf = (C.c_ulonglong * (16 * 1024))()
+    f(buf, 16 * 1024)
+    t = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(16, 1024)
+    t0 = t[t > 0].min()
+    t = np.where(t > 0, t - t0, -1)
+    for c in sorted(NAMES):
+        v = np.sort(t[c][t[c] >= 0])
+        if len(v) > 2:
+            print(f"{NAMES[c]:6s}: {len(v)} events, mean interval {np.diff(v).mean():.0f} cycles, span {v[-1]}")
+    # per-tile latencies (tile index g): S issue -> softmax has S -> P done -> PV issue
+    S, smS, smP, PV = t[4], t[7], t[8], t[6]
+    ok = (S >= 0) & (smS >= 0) & (smP >= 0) & (PV >= 0)
+    if ok.any():
+        print("tile: S->smS %.0f  smS->smP %.0f  smP->PV %.0f  (mean cycles over %d tiles)" % (
+            (smS - S)[ok].mean(), (smP - smS)[ok].mean(), (PV - smP)[ok].mean(), ok.sum()))
+    q, e0, e1 = t[1], t[9], t[10]
+    ok = (e0 >= 0) & (e1 >= 0)
+    if ok.any():
+        print("item epilogue %.0f cycles (mean over %d items)" % ((e1 - e0)[ok].mean(), ok.sum()))
 
 
 if __name__ == "__main__":
