@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Wno-deprecated-gpu-targets", "-I", os.path.join(ROOT, "include")]
-CU_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr"]
+CU_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr"] + os.environ.get("RX_NVCC_FLAGS", "").split()
 
 
 def _sources():

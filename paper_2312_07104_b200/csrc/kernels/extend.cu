@@ -53,6 +53,9 @@ constexpr int kExtThreads = 256;
 
 constexpr int kBN = 128;            // kv tokens per tile
 constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
+#ifndef RX_FENCE
+#define RX_FENCE 1
+#endif
 
 // Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
 // stores clock64 per (event code, item/tile index); read back with rx_debug_ext_trace().
@@ -311,61 +314,74 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
-      constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
-      int it = 0, jg = 0;
-      ExtItem I;
-      RingCursor rc;
-      while (ring_pop(I, rc, ring, desc_full, desc_empty, true)) {
-        const int qb = it & 1;
-        const uint32_t qa = sq + qb * C::Q_BYTES;
-        const uint32_t t_o = tmem + C::O_COL + qb * HD;
-        mbar_wait(q_full + qb, (it >> 1) & 1);
-        if (it >= 2) mbar_wait(o_free + qb, ((it >> 1) - 1) & 1);  // epilogue of item it-2 read O[qb]
-        auto issue_s = [&](int j) {
-          const int g_ = jg + j;
-          const int st = g_ % C::KS;
-          mbar_wait(k_full + st, (g_ / C::KS) & 1);
-          tc_fence_after();
-          fence_proxy_async();   // cp.async (generic-proxy) writes -> visible to the MMA (async proxy)
-          const uint32_t kb = sk + st * C::KV_BYTES;
-          const uint32_t t_s = tmem + (g_ & 1) * 128;
+    // The whole warp walks the loop (converged, warp-uniform operands: see
+    // elect_one); one elected lane issues each tcgen05.mma / commit.
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
+    int it = 0, jg = 0;
+    ExtItem I;
+    RingCursor rc;
+    while (ring_pop(I, rc, ring, desc_full, desc_empty, lane == 0)) {
+      const int n_tiles = __shfl_sync(0xffffffffu, I.n_tiles, 0);   // uniform for ptxas
+      const int qb = it & 1;
+      const uint32_t qa = sq + qb * C::Q_BYTES;
+      const uint32_t t_o = tmem + C::O_COL + qb * HD;
+      mbar_wait(q_full + qb, (it >> 1) & 1);
+      if (it >= 2) mbar_wait(o_free + qb, ((it >> 1) - 1) & 1);  // epilogue of item it-2 read O[qb]
+      auto issue_s = [&](int j) {
+        const int g_ = jg + j;
+        const int st = g_ % C::KS;
+        if (lane == 0) ext_trace(p.trace, 15, g_);
+        mbar_wait(k_full + st, (g_ / C::KS) & 1);
+        if (lane == 0) ext_trace(p.trace, 11, g_);
+        tc_fence_after();
+        if (RX_FENCE) fence_proxy_async();   // cp.async (generic-proxy) writes -> visible to the MMA (async proxy)
+        const uint32_t kb = sk + st * C::KV_BYTES;
+        const uint32_t t_s = tmem + (g_ & 1) * 128;
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
             const uint32_t off = (k >> 2) * 128 * kTileRowBytes + (k & 3) * 32;
             umma_ss(t_s, umma_desc_sw128(qa + off, 16, 1024),
                     umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
           }
+          ext_trace(p.trace, 13, g_);
           tc_commit(s_full + (g_ & 1));
           ext_trace(p.trace, 4, g_);
           tc_commit(k_empty + st);                          // K_g is free once S_g retires
-          if (j == I.n_tiles - 1) tc_commit(q_empty + qb);  // last read of this Q buffer issued
-        };
-        issue_s(0);
-        for (int j = 0; j < I.n_tiles; ++j) {
-          if (j + 1 < I.n_tiles) issue_s(j + 1);
-          const int g_ = jg + j;
-          mbar_wait(p_full + (g_ & 1), (g_ >> 1) & 1);
-          ext_trace(p.trace, 5, g_);
-          tc_fence_after();
-          const int st = g_ % C::VS;
-          mbar_wait(v_full + st, (g_ / C::VS) & 1);
-          fence_proxy_async();
-          const uint32_t vb = sv_ + st * C::KV_BYTES;
-          const uint32_t t_p = tmem + (g_ & 1) * 128;
+          if (j == n_tiles - 1) tc_commit(q_empty + qb);    // last read of this Q buffer issued
+        }
+        __syncwarp();
+      };
+      issue_s(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s(j + 1);
+        const int g_ = jg + j;
+        mbar_wait(p_full + (g_ & 1), (g_ >> 1) & 1);
+        if (lane == 0) ext_trace(p.trace, 5, g_);
+        tc_fence_after();
+        const int st = g_ % C::VS;
+        mbar_wait(v_full + st, (g_ / C::VS) & 1);
+        if (lane == 0) ext_trace(p.trace, 12, g_);
+        if (RX_FENCE) fence_proxy_async();
+        const uint32_t vb = sv_ + st * C::KV_BYTES;
+        const uint32_t t_p = tmem + (g_ & 1) * 128;
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kBN / 16; ++k)
             umma_ts(t_o, t_p + k * 8, umma_desc_sw128(vb + k * 2048, kBN * kTileRowBytes, 1024), idesc_o,
                     (j > 0 || k > 0) ? 1u : 0u);
+          ext_trace(p.trace, 14, g_);
           tc_commit(v_empty + st);
           tc_commit(o_done);
           ext_trace(p.trace, 6, g_);
         }
-        tc_commit(o_ready + qb);
-        jg += I.n_tiles;
-        ++it;
+        __syncwarp();
       }
+      if (elect_one()) tc_commit(o_ready + qb);
+      __syncwarp();
+      jg += n_tiles;
+      ++it;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue

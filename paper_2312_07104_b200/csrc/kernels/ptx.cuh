@@ -153,6 +153,15 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+// true on exactly one lane of the (converged) warp.  Issue tcgen05.mma / commit
+// under this from warp-converged code whose operands are warp-uniform: ptxas then
+// keeps them in uniform registers; under `if (lane == 0)` it cannot prove
+// uniformity and wraps every MMA in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t is = 0;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(is));
+  return is != 0;
+}
 // D[tmem] (+)= A[smem desc] * B[smem desc]
 __device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                         uint32_t accumulate) {

@@ -2,7 +2,8 @@
 
     RX_EXT_TRACE=1 python scripts/ext_trace.py --h 32 8 128 --batch 256 --prefix 0 --ext 384
 Codes: 1 Q issued, 2 K tile issued, 3 V tile issued, 4 S issued, 5 P seen by MMA, 6 PV issued,
-       7 softmax has S, 8 softmax P done, 9 epilogue start, 10 epilogue end.
+       7 softmax has S, 8 softmax P done, 9 epilogue start, 10 epilogue end, 11 K landed (seen by
+       the MMA warp), 12 V landed, 13 S MMAs issued, 14 PV MMAs issued, 15 MMA warp waits for K.
 """
 import argparse
 import ctypes as C
@@ -18,7 +19,8 @@ import torch
 import paper_2312_07104_b200 as rx
 from paper_2312_07104_b200._lib import lib
 
-NAMES = {1: "Q", 2: "K", 3: "V", 4: "S", 5: "Pseen", 6: "PV", 7: "smS", 8: "smP", 9: "epi0", 10: "epi1"}
+NAMES = {1: "Q", 2: "K", 3: "V", 4: "S", 5: "Pseen", 6: "PV", 7: "smS", 8: "smP", 9: "epi0", 10: "epi1",
+         11: "Kin", 12: "Vin", 13: "Smma", 14: "PVmma", 15: "Kwait"}
 
 
 def main():
@@ -27,6 +29,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--prefix", type=int, default=0)
     ap.add_argument("--ext", type=int, default=384)
+    ap.add_argument("--tiles", type=int, nargs=2, default=None, help="print per-tile event times for tiles [a, b)")
+    ap.add_argument("--log", type=int, nargs=2, default=None, help="time-ordered event log of tiles [a, b)")
     a = ap.parse_args()
     h_q, h_kv, hd = a.h
     B, P, E = a.batch, a.prefix, a.ext
@@ -67,6 +71,18 @@ def main():
     if ok.any():
         print("tile: S->smS %.0f  smS->smP %.0f  smP->PV %.0f  (mean cycles over %d tiles)" % (
             (smS - S)[ok].mean(), (smP - smS)[ok].mean(), (PV - smP)[ok].mean(), ok.sum()))
+    if a.tiles:
+        codes = [2, 3, 11, 4, 7, 8, 5, 12, 6]
+        print("tile " + " ".join(f"{NAMES[c]:>7s}" for c in codes) + "   (cycles since the tile's K issue)")
+        for g in range(*a.tiles):
+            z = t[2][g]
+            print(f"{g:4d} " + " ".join(f"{(t[c][g] - z) if t[c][g] >= 0 else -1:7d}" for c in codes))
+    if a.log:
+        ev = [(t[c][g], NAMES[c], g) for g in range(*a.log) for c in NAMES if c not in (1, 9, 10) and t[c][g] >= 0]
+        ev.sort()
+        z = ev[0][0]
+        for tt, n, g in ev:
+            print(f"{tt - z:8d}  {n:6s} tile {g}")
     q, e0, e1 = t[1], t[9], t[10]
     ok = (e0 >= 0) & (e1 >= 0)
     if ok.any():
