@@ -166,6 +166,38 @@ rx_status rx_finish_batch(rx_cache* c, int32_t batch, const rx_node* nodes, cons
                           const int64_t* offsets, const int32_t* slots, int64_t* d_evict,
                           int64_t* new_cached, int64_t* dup_freed);
 
+/* Cache-aware admission: Alg. 1 lines P:522-547 (§3 "Cache-aware scheduling",
+ * P:214-219) for one scheduling step, in one call.
+ *  1. rx_match_prefix_batch over the waiting queue (request b = prompt
+ *     tokens[offsets[b] .. offsets[b+1]), length >= 1, in arrival order) ->
+ *     nodes[b], matched[b], slots_out (nullable, same layout as tokens).
+ *  2. Order the queue by `policy`:
+ *       RX_SCHED_LSPF   longest matched prefix first ("longest-shared-prefix-
+ *                       first"; optimal by Theorem 1),
+ *                       ties by arrival;
+ *       RX_SCHED_FCFS   arrival order (ablation);
+ *       RX_SCHED_RANDOM ascending keys[b] (uint64, caller-drawn: the random
+ *                       numbers are an input), ties by arrival (ablation).
+ *  3. Admit in that order while size_b + current < available + delta_b
+ *     (strict), available = evictable + free grown by each
+ *     admitted request's rx_inc_ref delta, delta_b = request b's
+ *     own pin delta (reading R25: b is pinned, tested, and unpinned again if
+ *     it does not fit), current += size_b (reading R7),
+ *     size_b = (n_b - min(matched_b, n_b - 1)) + max_new[b] (R7, R11).
+ *     Admitted requests stay pinned (rx_inc_ref on nodes[b]).
+ * Outputs: admitted[0 .. *n_admitted) = request indices in admission order
+ * (caller capacity >= batch); deltas[k] (nullable) = inc_ref delta of the
+ * k-th admitted request.  Nothing is allocated: the caller allocates the
+ * batch's slots (rx_alloc_evict) and later calls rx_finish_batch.
+ * Errors: RX_E_INVALID for a null required pointer, an empty prompt, a
+ * negative max_new, an unknown policy, or RANDOM without keys (checked before
+ * any side effect); a tree error stops the call and is returned. */
+typedef enum { RX_SCHED_LSPF = 0, RX_SCHED_FCFS = 1, RX_SCHED_RANDOM = 2 } rx_sched_policy;
+rx_status rx_schedule(rx_cache* c, int32_t batch, const int32_t* tokens, const int64_t* offsets,
+                      const int64_t* max_new, int32_t policy, const uint64_t* keys, rx_node* nodes,
+                      int64_t* matched, int32_t* slots_out, int32_t* admitted, int32_t* n_admitted,
+                      int64_t* deltas);
+
 /* Pure queries (Alg. 1 "T.evictable_size() + P.available_size()", P:534;
  * SPEC S:149-156).  evictable = tokens on non-root nodes with ref 0 (pins
  * propagate to the root, so these are exactly the peelable nodes). */

@@ -61,10 +61,11 @@ class Seq:
 
 
 class OracleEngine:
-    def __init__(self, wl, sample_extend=None, sample_decode=None, q_scale=1.0, materialize=False):
+    def __init__(self, wl, sample_extend=None, sample_decode=None, q_scale=1.0, materialize=False, policy="lspf"):
         """sample_extend(call_idx, B, prefix_lens, extend_lens) -> list of (req_idx, j) rows to evaluate, or None (= none);
         sample_decode(call_idx, step, B) -> list of req_idx to evaluate."""
         self.wl = wl
+        self.policy = policy        # Alg. 1 queue order (P:218 "lspf"; P:432 ablations "fcfs", "random")
         self.shape = wl.shape
         self.tree = RadixCache(wl.num_slots)
         self.slot_hash = {}
@@ -158,35 +159,56 @@ class OracleEngine:
     def run_waves(self, reqs):
         """Alg. 1 admission repeated until every request has run.
 
-        Each wave: match every waiting request, sort by matched length
-        (longest first, ties by arrival), admit while req.size() + current <
-        available with available = evictable + free updated by the
-        inc_ref delta and current += req.size() (R7); req.size()
-        = new prompt tokens + max_new_tokens.  The admitted batch runs to
-        completion (reading R22: waves instead of per-iteration joins)."""
+        Each wave: match every waiting request, sort the queue by
+        self.policy — "lspf": matched length, longest first, ties by arrival
+        (P:218); "fcfs": arrival order; "random": ascending rxgen.sched_keys,
+        ties by arrival (the ablations of P:432) — then admit while
+        req.size() + current < available + delta with available = evictable +
+        free updated by the inc_ref delta, delta = the
+        candidate's own pin delta (R25), and current += req.size() (R7);
+        req.size() = new prompt tokens + max_new_tokens.  The
+        admitted batch runs to completion (reading R22: waves instead of
+        per-iteration joins)."""
+        from rxgen import sched_keys
         waiting = self._seqs(reqs)
         done = []
+        wave = 0
         while waiting:
             self._match(waiting)
-            order = sorted(range(len(waiting)), key=lambda i: (-waiting[i].matched, i))
+            idx = list(range(len(waiting)))
+            if self.policy == "lspf":
+                order = sorted(idx, key=lambda i: (-waiting[i].matched, i))
+            elif self.policy == "fcfs":
+                order = idx
+            elif self.policy == "random":
+                keys = [int(k) for k in sched_keys(self.wl.seed, wave, len(waiting))]
+                order = sorted(idx, key=lambda i: (keys[i], i))
+            else:
+                raise ValueError(self.policy)
             available = self.tree.evictable_size() + self.tree.available()
             current = 0
             admitted = []
             for i in order:
                 s = waiting[i]
                 size = (s.n_prompt - s.prefix_len) + s.n_out
-                if size + current < available:
-                    d = self.tree.inc_ref(s.node)
+                # reading R25: the fit check counts the candidate's own pin (Alg. 1 checks
+                # before pinning, which lets a later pin shrink `available` below what the
+                # already-admitted requests need)
+                d = self.tree.inc_ref(s.node)
+                if size + current < available + d:
                     self.trace.append(("inc_ref", s.rid, d))
                     available += d
                     current += size
                     admitted.append(i)
+                else:
+                    self.tree.dec_ref(s.node)
             if not admitted:
                 raise OOM("no waiting request fits the pool")
             self.trace.append(("admit", tuple(waiting[i].rid for i in admitted)))
             done.extend(self._run_matched([waiting[i] for i in admitted]))
             keep = set(admitted)
             waiting = [s for i, s in enumerate(waiting) if i not in keep]
+            wave += 1
         by_rid = {s.rid: s for s in done}
         return [by_rid[r.tag] for r in reqs]
 
@@ -249,7 +271,10 @@ class OracleEngine:
         if wl.name == "C4":
             return self._run_tot()
         for kind, reqs in wl.phases:
-            self.run_batch(reqs)
+            if kind == "queue":
+                self.run_waves(reqs)
+            else:
+                self.run_batch(reqs)
         return self
 
     def _run_chat(self):

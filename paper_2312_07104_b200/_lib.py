@@ -59,6 +59,8 @@ SIGNATURES = {
     "rx_match_prefix_batch": (C.c_int, [vp, i32, P32, P64, P64, P64, P32]),
     "rx_inc_ref_batch": (C.c_int, [vp, i32, P64, P64]),
     "rx_finish_batch": (C.c_int, [vp, i32, P64, P32, P64, P32, P64, P64, P64]),
+    "rx_schedule": (C.c_int, [vp, i32, P32, P64, P64, i32, C.POINTER(C.c_uint64), P64, P64, P32, P32,
+                              C.POINTER(i32), P64]),
     "rx_evictable_size": (i64, [vp]),
     "rx_total_cached": (i64, [vp]),
     "rx_available": (i64, [vp]),

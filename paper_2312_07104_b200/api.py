@@ -16,6 +16,7 @@ import numpy as np
 from ._lib import lib, AttnCfg, EVICT_CB, EVICT_PATH_CB, RxError, P32, P64
 
 _I32 = np.int32
+SCHED_POLICY = {"lspf": 0, "fcfs": 1, "random": 2}   # rx_sched_policy
 
 
 def _i32(a) -> np.ndarray:
@@ -160,6 +161,27 @@ class RadixCache:
                                    d.ctypes.data_as(P64), nc.ctypes.data_as(P64), nd.ctypes.data_as(P64)),
                "rx_finish_batch")
         return d, nc, nd
+
+    def rx_schedule(self, tokens_concat, offsets, max_new, policy="lspf", keys=None):
+        """Alg. 1 admission step -> (nodes int64[B], matched int64[B], slots int32 (tokens layout),
+        admitted int32[k] in admission order, deltas int64[k])."""
+        t = _i32(tokens_concat)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        B = len(off) - 1
+        mn = np.ascontiguousarray(max_new, dtype=np.int64)
+        pol = SCHED_POLICY[policy]
+        kp = None
+        if keys is not None:
+            keys = np.ascontiguousarray(keys, dtype=np.uint64)
+            kp = keys.ctypes.data_as(C.POINTER(C.c_uint64))
+        nodes, matched = np.empty(B, dtype=np.int64), np.empty(B, dtype=np.int64)
+        slots = np.empty(max(len(t), 1), dtype=_I32)
+        adm, d = np.empty(max(B, 1), dtype=_I32), np.empty(max(B, 1), dtype=np.int64)
+        k = C.c_int32(0)
+        _check(lib.rx_schedule(self._h, B, _p32(t), off.ctypes.data_as(P64), mn.ctypes.data_as(P64), pol, kp,
+                               nodes.ctypes.data_as(P64), matched.ctypes.data_as(P64), _p32(slots), _p32(adm),
+                               C.byref(k), d.ctypes.data_as(P64)), "rx_schedule")
+        return nodes, matched, slots, adm[:k.value].copy(), d[:k.value].copy()
 
     def rx_evictable_size(self) -> int:
         return lib.rx_evictable_size(self._h)

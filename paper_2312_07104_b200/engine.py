@@ -100,8 +100,9 @@ class InputBank:
 
 class Engine:
     def __init__(self, wl, device="cuda", tp_rank=0, tp_size=1, plan_only=False, record=False,
-                 keep_outputs=False, gather=None, cascade=True):
+                 keep_outputs=False, gather=None, cascade=True, policy="lspf"):
         self.wl = wl
+        self.policy = policy                  # Alg. 1 queue order: "lspf" (paper), "fcfs", "random"
         self.shape = wl.shape
         self.device = device
         self.plan_only = plan_only
@@ -205,28 +206,33 @@ class Engine:
     def run_waves(self, reqs):
         """Alg. 1 admission (R7) repeated until every request ran (waves, R22).
 
-        Sort by matched length (longest first, ties by arrival); admit while
-        size + current < available, available = evictable + free updated by
-        the inc_ref delta, current += size, size = new prompt tokens + max_new."""
+        One rx_schedule call per wave (library C++): match every waiting request, order the queue by
+        self.policy (LSPF = longest matched prefix first, ties by arrival; FCFS; RANDOM with keys
+        from rxgen.sched_keys), admit while size + current < available, available = evictable +
+        free updated by the inc_ref delta, current += size, size = new prompt tokens + max_new."""
+        from rxgen import sched_keys
         c = self.cache
         waiting = self._reqs(reqs)
         done = {}
+        wave = 0
         while waiting:
             t0 = time.perf_counter()
-            self._match(waiting)
-            order = sorted(range(len(waiting)), key=lambda i: (-waiting[i].matched, i))
-            available = c.rx_evictable_size() + c.rx_available()
-            current = 0
-            admitted = []
-            for i in order:
-                r = waiting[i]
-                size = (r.n_prompt - r.prefix) + r.n_out
-                if size + current < available:
-                    d = c.rx_inc_ref(r.node)
-                    self._rec("inc_ref", r.rid, d)
-                    available += d
-                    current += size
-                    admitted.append(i)
+            toks = np.concatenate([r.tokens[:r.n_prompt] for r in waiting])
+            off = np.zeros(len(waiting) + 1, dtype=np.int64)
+            off[1:] = np.cumsum([r.n_prompt for r in waiting])
+            keys = sched_keys(self.wl.seed, wave, len(waiting)) if self.policy == "random" else None
+            nodes, matched, sl, adm, deltas = c.rx_schedule(toks, off, [r.n_out for r in waiting], self.policy, keys)
+            for b, r in enumerate(waiting):
+                m = int(matched[b])
+                if self.record:
+                    self._rec("match", r.rid, m, tuple(int(x) for x in sl[off[b]:off[b] + m]))
+                r.node = int(nodes[b])
+                r.matched = m
+                r.prefix = min(m, r.n_prompt - 1)
+                r.slots = sl[off[b]:off[b] + r.prefix]
+            admitted = [int(i) for i in adm]
+            for i, d in zip(admitted, deltas):
+                self._rec("inc_ref", waiting[i].rid, int(d))
             if not admitted:
                 raise OutOfSlots("no waiting request fits the pool")
             self._rec("admit", tuple(waiting[i].rid for i in admitted))
@@ -235,6 +241,7 @@ class Engine:
                 done[r.rid] = r
             keep = set(admitted)
             waiting = [r for i, r in enumerate(waiting) if i not in keep]
+            wave += 1
         return [done[q.tag] for q in reqs]
 
     def _run_matched(self, rs):
@@ -490,7 +497,10 @@ class Engine:
         if wl.name == "C4":
             return self._run_tot()
         for kind, reqs in wl.phases:
-            self.run_batch(reqs)
+            if kind == "queue":
+                self.run_waves(reqs)
+            else:
+                self.run_batch(reqs)
         return self
 
     def _run_chat(self):
@@ -517,9 +527,9 @@ class Engine:
         return self
 
 
-def plan_and_bank(wl, device="cuda", tp_rank=0, tp_size=1, q_scale=1.0):
+def plan_and_bank(wl, device="cuda", tp_rank=0, tp_size=1, q_scale=1.0, policy="lspf"):
     """Plan pass + input generation (untimed setup).  Returns (plan engine, InputBank)."""
-    plan = Engine(wl, device=device, tp_rank=tp_rank, tp_size=tp_size, plan_only=True)
+    plan = Engine(wl, device=device, tp_rank=tp_rank, tp_size=tp_size, plan_only=True, policy=policy)
     plan.run_workload()
     bank = InputBank(plan.calls, wl.shape, plan.heads_q, plan.heads_kv, device, q_scale=q_scale)
     return plan, bank

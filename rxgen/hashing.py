@@ -74,3 +74,10 @@ def extend_hashes(h_prev: int, tokens) -> np.ndarray:
 def next_token(h: int, vocab: int) -> int:
     """Mock model: the token generated after a prefix whose hash is h."""
     return 1 + splitmix64_int((h ^ NEXT_SALT) & MASK64) % (vocab - 1)
+
+
+def sched_keys(seed: int, wave: int, n: int) -> np.ndarray:
+    """Random-schedule priority keys (the P:432 "Random Schedule" ablation): key i of a wave is
+    splitmix64(seed ^ (wave << 32) ^ i).  An input, drawn identically for the oracle and the library."""
+    x = np.arange(n, dtype=np.uint64) ^ np.uint64((int(seed) ^ (int(wave) << 32)) & MASK64)
+    return splitmix64_np(x)

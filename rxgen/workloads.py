@@ -142,4 +142,23 @@ def c5(seed: int = 0, n_req: int = 128, prefix: int = 8192, question: int = 128,
                     {"prefix": prefix, "decode": decode})
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
+def mix(seed: int = 0, groups: int = 4, per_group: int = 16, prefix: int = 1024, q_lo: int = 32, q_hi: int = 96,
+        out_lo: int = 8, out_hi: int = 32, num_slots: int = 2600) -> Workload:
+    """Scheduling ablation ("FCFS / Random Schedule"): `groups` unrelated few-shot
+    prefixes, per_group questions each, arriving interleaved (request i belongs to group i mod groups)
+    in ONE waiting queue; the pool holds roughly 1.5 groups, so the admission order decides how often
+    a prefix is evicted and recomputed (cache thrashing).  Llama-2-7B attention shape (32/32/128), no
+    hint requests.  Phase kind "queue" = Alg. 1 admission waves over the whole queue."""
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    pres = [_rand_tokens(rng, prefix, vocab) for _ in range(groups)]
+    reqs = []
+    for i in range(groups * per_group):
+        g = i % groups
+        q = _rand_tokens(rng, int(rng.integers(q_lo, q_hi + 1)), vocab)
+        reqs.append(Request(np.concatenate([pres[g], q]), int(rng.integers(out_lo, out_hi + 1)), f"g{g}r{i}"))
+    return Workload("MIX", Shape(32, 32, 128), num_slots, vocab, seed, [("queue", reqs)],
+                    {"groups": groups, "prefix": prefix})
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "MIX": mix}

@@ -21,9 +21,9 @@ if torch.cuda.is_available():
 MAX_ABS, MEAN_ABS = 2e-2, 2e-3
 
 
-def _run_gpu(wl, q_scale=1.0):
-    plan, bank = plan_and_bank(wl, "cuda", q_scale=q_scale)
-    e = Engine(wl, "cuda", record=True, keep_outputs=True)
+def _run_gpu(wl, q_scale=1.0, policy="lspf"):
+    plan, bank = plan_and_bank(wl, "cuda", q_scale=q_scale, policy=policy)
+    e = Engine(wl, "cuda", record=True, keep_outputs=True, policy=policy)
     e.run_workload(bank)
     torch.cuda.synchronize()
     return e
@@ -36,7 +36,7 @@ def _outputs_by_key(e):
     return ext, dec
 
 
-def _compare(o_eng, wl, rows_ext, rows_dec, q_scale=1.0):
+def _compare(o_eng, wl, rows_ext, rows_dec, q_scale=1.0, policy="lspf"):
     ext_s = {}
     dec_s = {}
 
@@ -47,7 +47,7 @@ def _compare(o_eng, wl, rows_ext, rows_dec, q_scale=1.0):
         return rows_dec(call, step, running)
 
     small = wl.num_slots * wl.shape.h_kv * wl.shape.head_dim <= (1 << 26)
-    oe = OracleEngine(wl, sample_extend=se, sample_decode=sd, q_scale=q_scale, materialize=small)
+    oe = OracleEngine(wl, sample_extend=se, sample_decode=sd, q_scale=q_scale, materialize=small, policy=policy)
     oe.run_workload()
     ext, dec = _outputs_by_key(o_eng)
     errs = []
@@ -130,5 +130,17 @@ def test_c4_tot_full_parity():
     oe = _compare(e, wl, lambda c, seqs: [(i, j) for i, s in enumerate(seqs)
                                           for j in range(s.n_prompt - s.prefix_len) if j % 7 == 0 or c > 0],
                   _all_dec)
+    assert oe.trace == e.trace
+    assert any(t[0] == "evict" for t in e.trace)
+
+
+@pytest.mark.parametrize("policy", ["lspf", "fcfs", "random"])
+def test_mix_schedule_parity(policy):
+    """Scheduling ablation queue (interleaved few-shot groups, pool < the groups' prefixes):
+    admission by rx_schedule under each policy, evictions and prefix recomputation between waves;
+    tree trace bit-exact and every attention row within tolerance."""
+    wl = workloads.mix(groups=3, per_group=6, prefix=300, q_lo=20, q_hi=60, out_lo=2, out_hi=6, num_slots=900)
+    e = _run_gpu(wl, policy=policy)
+    oe = _compare(e, wl, _all_ext, _all_dec, policy=policy)
     assert oe.trace == e.trace
     assert any(t[0] == "evict" for t in e.trace)
