@@ -214,6 +214,39 @@ int64_t rx_clock(const rx_cache* c);
 int64_t rx_dump_json(const rx_cache* c, char* buf, int64_t cap);
 
 /* ----------------------------------------------------------------------- */
+/*  Compressed FSM for constrained decoding (§4, App. B; */
+/*  SURVEY §8(f) NEXT-4).  Host only.                                       */
+/* ----------------------------------------------------------------------- */
+/* "converting a regular expression into a finite state machine":
+ * rx_fsm_create parses regex[0..len) (ASCII; literals, escapes \d \w \s \n
+ * \t and escaped punctuation, classes [..] with ranges and ^, '.', groups,
+ * '|', quantifiers * + ? {m} {m,} {m,n}) and builds the MINIMAL DFA over
+ * bytes 0..127, dead states removed, states numbered breadth-first from the
+ * start state (0) by ascending byte (reading R27; the numbering is unique).
+ * RX_E_INVALID on a syntax error or an empty language (no side effect);
+ * RX_E_NOMEM on allocation failure.  The vocabulary is byte-level (R26).
+ * Queries return -1 for a bad handle/state/byte:
+ *   rx_fsm_step        next state after `byte`, or -1 if not allowed;
+ *   rx_fsm_is_accepting 1 if the model may stop at `state`;
+ *   rx_fsm_allowed     number of allowed bytes; out (nullable, cap >= 128)
+ *                      receives them ascending;
+ *   rx_fsm_jump        "Jump Forward" along the compressed edge
+ *                      (adjacent singular transitions merged): while
+ *                      `state` has exactly one allowed byte and is not
+ *                      accepting, emit that byte and move; returns the number
+ *                      of bytes (0 if `state` is not singular), out (nullable)
+ *                      receives them, *end_state (nullable) the state reached;
+ *                      -1 if cap is too small. */
+typedef struct rx_fsm rx_fsm;
+rx_status rx_fsm_create(const char* regex, int64_t len, rx_fsm** out);
+void rx_fsm_destroy(rx_fsm* f);
+int32_t rx_fsm_num_states(const rx_fsm* f);
+int32_t rx_fsm_step(const rx_fsm* f, int32_t state, int32_t byte);
+int32_t rx_fsm_is_accepting(const rx_fsm* f, int32_t state);
+int32_t rx_fsm_allowed(const rx_fsm* f, int32_t state, uint8_t* out);
+int32_t rx_fsm_jump(const rx_fsm* f, int32_t state, uint8_t* out, int32_t cap, int32_t* end_state);
+
+/* ----------------------------------------------------------------------- */
 /*  Data-parallel router (App. A.4)          */
 /* ----------------------------------------------------------------------- */
 /* "each worker maintains its own sub-tree, while the router oversees a

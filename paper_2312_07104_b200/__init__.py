@@ -5,11 +5,11 @@ sm_100a kernels for KV store, extend (tcgen05/TMEM) and decode (split-KV,
 GQA-grouped).  This package is the thin Python binding plus the request-flow
 harness that drives it.  It never imports ``oracle/``.
 """
-from .api import (RadixCache, attn_cfg, rx_store_kv, rx_extend, rx_decode, rx_decode_append, rx_decode_cascade_append,
+from .api import (RadixCache, Fsm, attn_cfg, rx_store_kv, rx_extend, rx_decode, rx_decode_append, rx_decode_cascade_append,
                   rx_decode_cascade_workspace_bytes, rx_extend_workspace_bytes,
                   rx_decode_workspace_bytes, rx_last_launch_count)
 from ._lib import RxError, LIB_PATH
 
-__all__ = ["RadixCache", "attn_cfg", "rx_store_kv", "rx_extend", "rx_decode", "rx_decode_append", "rx_decode_cascade_append",
+__all__ = ["RadixCache", "Fsm", "attn_cfg", "rx_store_kv", "rx_extend", "rx_decode", "rx_decode_append", "rx_decode_cascade_append",
            "rx_decode_cascade_workspace_bytes", "rx_extend_workspace_bytes",
            "rx_decode_workspace_bytes", "rx_last_launch_count", "RxError", "LIB_PATH"]

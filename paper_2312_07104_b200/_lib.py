@@ -61,6 +61,13 @@ SIGNATURES = {
     "rx_finish_batch": (C.c_int, [vp, i32, P64, P32, P64, P32, P64, P64, P64]),
     "rx_schedule": (C.c_int, [vp, i32, P32, P64, P64, i32, C.POINTER(C.c_uint64), P64, P64, P32, P32,
                               C.POINTER(i32), P64]),
+    "rx_fsm_create": (C.c_int, [C.c_char_p, i64, C.POINTER(vp)]),
+    "rx_fsm_destroy": (None, [vp]),
+    "rx_fsm_num_states": (i32, [vp]),
+    "rx_fsm_step": (i32, [vp, i32, i32]),
+    "rx_fsm_is_accepting": (i32, [vp, i32]),
+    "rx_fsm_allowed": (i32, [vp, i32, C.POINTER(C.c_uint8)]),
+    "rx_fsm_jump": (i32, [vp, i32, C.POINTER(C.c_uint8), i32, C.POINTER(i32)]),
     "rx_evictable_size": (i64, [vp]),
     "rx_total_cached": (i64, [vp]),
     "rx_available": (i64, [vp]),

@@ -202,6 +202,47 @@ class RadixCache:
         return json.loads(buf.value.decode())
 
 
+class Fsm:
+    """rx_fsm: minimal DFA of a regex with compressed (singular) edges (§4, App. B)."""
+
+    def __init__(self, regex: str):
+        b = regex.encode("ascii")
+        h = C.c_void_p()
+        _check(lib.rx_fsm_create(b, len(b), C.byref(h)), "rx_fsm_create")
+        self._h = h
+        self.num_states = lib.rx_fsm_num_states(h)
+        self._buf = (C.c_uint8 * 128)()
+
+    def close(self):
+        if self._h:
+            lib.rx_fsm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rx_fsm_step(self, state: int, byte: int) -> int:
+        return lib.rx_fsm_step(self._h, state, byte)
+
+    def rx_fsm_is_accepting(self, state: int) -> bool:
+        return lib.rx_fsm_is_accepting(self._h, state) == 1
+
+    def rx_fsm_allowed(self, state: int):
+        k = lib.rx_fsm_allowed(self._h, state, self._buf)
+        return list(self._buf[:k])
+
+    def rx_fsm_jump(self, state: int):
+        """-> (forced bytes, end state)"""
+        n = lib.rx_fsm_jump(self._h, state, None, 1 << 30, None)
+        buf = (C.c_uint8 * max(n, 1))()
+        end = C.c_int32()
+        n = lib.rx_fsm_jump(self._h, state, buf, n, C.byref(end))
+        return list(buf[:n]), end.value
+
+
 class Router:
     """rx_router: the data-parallel meta-tree router (App. A.4)."""
 
