@@ -212,6 +212,100 @@ class OracleEngine:
         by_rid = {s.rid: s for s in done}
         return [by_rid[r.tag] for r in reqs]
 
+    # ------------------------------------------------------------ constrained decoding (§4)
+    def run_fsm_batch(self, reqs):
+        """A batch decoding under the workload's regex, admitted whole.
+
+        §4 P:255-266 / App. B, step by step.  The FSM (oracle.fsm, built once for the
+        batch) walks with the mock model (rxgen.fsm_choice, R28): at a state the options are
+        the allowed bytes, ascending, then STOP if the state is accepting.  Compressed mode: at a
+        singular state the whole compressed edge is appended at once (Jump Forward) — from
+        the start state it is prefilled with the prompt; after a sampled token it is processed in
+        the same forward pass as that token ("decoded in one forward pass").  Normal mode:
+        one token per forward pass.  Each forward pass over more than one token of a
+        request is an extend call, otherwise a decode call; slots are allocated per pass in batch
+        order (R23); a request that chooses STOP finishes (dec_ref + insert) before the next pass."""
+        from rxgen import fsm_choice
+        from .fsm import FSM
+        if getattr(self, "_fsm", None) is None:
+            self._fsm = FSM(self.wl.meta["regex"])
+        fsm, compressed = self._fsm, self.wl.meta["compressed"]
+        seqs = self._seqs(reqs)
+        self._match(seqs)
+        for s in seqs:
+            self.trace.append(("inc_ref", s.rid, self.tree.inc_ref(s.node)))
+            self.stats["prompt_tokens"] += s.n_prompt
+            self.stats["cached_prompt_tokens"] += s.prefix_len
+
+        def append(s, byte):
+            t = byte + 1                              # byte-level vocabulary (R26)
+            s.tokens.append(t)
+            s.hashes.append(splitmix64_int((s.hashes[-1] ^ t) & MASK64))
+
+        for s in seqs:
+            s.state = 0
+            if compressed:
+                forced, s.state = fsm.jump(0)
+                for b in forced:
+                    append(s, b)
+        # prefill: prompt (beyond the cached prefix) + the start state's forced edge
+        ext = [len(s.tokens) - s.prefix_len for s in seqs]
+        new = self._alloc(sum(ext))
+        off = 0
+        for s, n in zip(seqs, ext):
+            s.slots.extend(new[off:off + n])
+            off += n
+        call = self.extend_calls
+        self.extend_calls += 1
+        self._store([s.slots[p] for s in seqs for p in range(s.prefix_len, len(s.tokens))],
+                    [s.hashes[p] for s in seqs for p in range(s.prefix_len, len(s.tokens))])
+        for (bi, j) in (self.sample_extend(call, seqs) if self.sample_extend else []):
+            if j < ext[bi]:
+                self.outputs[("extend", call, bi, j)] = self._attend(seqs[bi], seqs[bi].prefix_len + j)
+        running = seqs
+        step = 0
+        while running:
+            # the model's choice after the last processed token of every running request
+            still, seg = [], []
+            for s in running:
+                opts = fsm.allowed(s.state) + (["STOP"] if fsm.accepting[s.state] else [])
+                pick = opts[fsm_choice(s.hashes[-1], len(opts))]
+                if pick == "STOP":
+                    self._finish(s)
+                    continue
+                start = len(s.tokens)
+                append(s, pick)
+                s.state = fsm.step(s.state, pick)
+                if compressed:
+                    forced, s.state = fsm.jump(s.state)
+                    for b in forced:
+                        append(s, b)
+                still.append(s)
+                seg.append((start, len(s.tokens) - start))
+            running = still
+            if not running:
+                break
+            new = self._alloc(sum(n for _, n in seg))
+            off = 0
+            for s, (p0, n) in zip(running, seg):
+                s.slots.extend(new[off:off + n])
+                off += n
+            self._store(new, [s.hashes[p] for s, (p0, n) in zip(running, seg) for p in range(p0, p0 + n)])
+            if all(n == 1 for _, n in seg):
+                call = self.decode_calls
+                self.decode_calls += 1
+                for bi in (self.sample_decode(call, step, running) if self.sample_decode else []):
+                    self.outputs[("decode", call, bi)] = self._attend(running[bi], len(running[bi].tokens) - 1)
+            else:
+                call = self.extend_calls
+                self.extend_calls += 1
+                for (bi, j) in (self.sample_extend(call, running) if self.sample_extend else []):
+                    if j < seg[bi][1]:
+                        self.outputs[("extend", call, bi, j)] = self._attend(running[bi], seg[bi][0] + j)
+            step += 1
+        self.trace.append(("sizes", self.tree.evictable_size(), self.tree.total_cached(), self.tree.available()))
+        return seqs
+
     def _run_matched(self, seqs):
         for s in seqs:
             self.stats["prompt_tokens"] += s.n_prompt
@@ -273,6 +367,8 @@ class OracleEngine:
         for kind, reqs in wl.phases:
             if kind == "queue":
                 self.run_waves(reqs)
+            elif kind == "fsm":
+                self.run_fsm_batch(reqs)
             else:
                 self.run_batch(reqs)
         return self

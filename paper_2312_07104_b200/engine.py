@@ -50,12 +50,18 @@ def shard_heads(h_q: int, h_kv: int, rank: int, size: int):
 
 
 class _Req:
-    __slots__ = ("rid", "tokens", "hashes", "n_prompt", "n_out", "node", "prefix", "slots", "row", "matched")
+    __slots__ = ("rid", "tokens", "hashes", "n_prompt", "n_out", "node", "prefix", "slots", "row", "matched",
+                 "first", "segs")
 
-    def __init__(self, rid, prompt, n_out, seed, vocab, full=None):
+    def __init__(self, rid, prompt, n_out, seed, vocab, full=None, first=0, segs=None):
         self.rid = rid
         self.n_prompt = len(prompt)
         self.n_out = n_out
+        # output schedule: `first` output tokens ride along with the prompt's extend (a jump-forward
+        # edge at the FSM start), then one forward pass per segment of segs[k] tokens (1 = a decode
+        # step; > 1 = a sampled token plus its jump-forward edge, an extend step)
+        self.first = first
+        self.segs = np.ones(n_out - first, dtype=np.int64) if segs is None else np.asarray(segs, dtype=np.int64)
         if full is None:
             toks = [int(t) for t in prompt]
             hs = [int(h) for h in prefix_hashes(toks, seed)]
@@ -131,6 +137,8 @@ class Engine:
         self.cascade_min_len = 256
         self.cascade_min_batch = 4
         self._shared = 0
+        self._ws = None
+        self._fsm = None                      # compressed FSM of the workload's regex (JSON workload)
         if not plan_only:
             hd = wl.shape.head_dim
             self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
@@ -172,6 +180,66 @@ class Engine:
             self._full_cache[key] = (r.tokens, r.hashes)
             rs.append(r)
         return rs
+
+    def _fsm_reqs(self, reqs):
+        """Requests decoding under the workload's regex (§4): the output is the mock
+        model's walk of the compressed FSM (library rx_fsm_*, built once and reused for the batch,
+        P:442); compressed mode groups each sampled token with the jump-forward edge that follows
+        it, so one forward pass covers the whole segment."""
+        from rxgen import fsm_choice
+        wl = self.wl
+        if self._fsm is None:
+            self._fsm = api.Fsm(wl.meta["regex"])
+        fsm, compressed = self._fsm, wl.meta["compressed"]
+        rs = []
+        for q in reqs:
+            key = ("fsm", q.tag, len(q.prompt), compressed)
+            if key in self._full_cache:
+                toks, hs, first, segs = self._full_cache[key]
+            else:
+                toks = [int(t) for t in q.prompt]
+                hs = [int(h) for h in prefix_hashes(toks, wl.seed)]
+
+                def emit(byte):
+                    t = byte + 1                      # byte-level vocabulary (R26)
+                    hs.append(splitmix64_int((hs[-1] ^ t) & MASK64))
+                    toks.append(t)
+                st, first, segs = 0, 0, []
+                if compressed:
+                    forced, st = fsm.rx_fsm_jump(0)
+                    for b in forced:
+                        emit(b)
+                    first = len(forced)
+                while True:
+                    opts = fsm.rx_fsm_allowed(st) + ([-1] if fsm.rx_fsm_is_accepting(st) else [])
+                    pick = opts[fsm_choice(hs[-1], len(opts))]
+                    if pick < 0:                      # STOP
+                        break
+                    emit(pick)
+                    st = fsm.rx_fsm_step(st, pick)
+                    n = 1
+                    if compressed:
+                        forced, st = fsm.rx_fsm_jump(st)
+                        for b in forced:
+                            emit(b)
+                        n += len(forced)
+                    segs.append(n)
+                toks = np.asarray(toks, dtype=np.int32)
+                hs = np.asarray(hs, dtype=np.uint64)
+                self._full_cache[key] = (toks, hs, first, segs)
+            rs.append(_Req(q.tag, q.prompt, len(toks) - len(q.prompt), wl.seed, wl.vocab, (toks, hs), first, segs))
+        return rs
+
+    def run_fsm_batch(self, reqs):
+        """One batch of regex-constrained requests admitted whole (as run_batch)."""
+        t0 = time.perf_counter()
+        rs = self._fsm_reqs(reqs)
+        self._match(rs)
+        deltas = self.cache.rx_inc_ref_batch([r.node for r in rs])
+        for r, d in zip(rs, deltas):
+            self._rec("inc_ref", r.rid, int(d))
+        self.stats["tree_s"] += time.perf_counter() - t0
+        return self._run_matched(rs)
 
     def _match(self, rs):
         """match_prefix for every request (Alg. 1); usable prefix capped at n-1 (R11)."""
@@ -250,6 +318,7 @@ class Engine:
         c = self.cache
         n_prompt = np.array([r.n_prompt for r in rs], dtype=np.int64)
         n_out = np.array([r.n_out for r in rs], dtype=np.int64)
+        first = np.array([r.first for r in rs], dtype=np.int64)
         stride = int((n_prompt + n_out).max())
         slots = np.zeros((B, stride), dtype=np.int32)        # host mirror of this batch's req_to_token rows
         prefix = np.array([r.prefix for r in rs], dtype=np.int64)
@@ -257,11 +326,11 @@ class Engine:
             slots[b, :r.prefix] = r.slots
         self.stats["prompt_tokens"] += int(n_prompt.sum())
         self.stats["cached_prompt_tokens"] += int(prefix.sum())
-        ext = n_prompt - prefix
+        ext = n_prompt + first - prefix
         new = self._alloc(int(ext.sum()))
         off = 0
         for b in range(B):
-            slots[b, prefix[b]:n_prompt[b]] = new[off:off + ext[b]]
+            slots[b, prefix[b]:prefix[b] + ext[b]] = new[off:off + ext[b]]
             off += ext[b]
         self.stats["tree_s"] += time.perf_counter() - t0
         self._slots_host = slots
@@ -277,33 +346,59 @@ class Engine:
             self._shared = 0
         self._extend(rs, slots, prefix, ext)
         t0 = time.perf_counter()
-        self._finish_many(rs, np.nonzero(n_out == 0)[0], slots)
-        running = np.nonzero(n_out > 0)[0]
+        nseg = np.array([len(r.segs) for r in rs], dtype=np.int64)
+        self._finish_many(rs, np.nonzero(nseg == 0)[0], slots)
+        running = np.nonzero(nseg > 0)[0]
         self.stats["tree_s"] += time.perf_counter() - t0
-        # Decode phase, in two passes.  (A) every tree op of the phase — one slot per running request
-        # per step (R23), finished requests' dec_ref + insert — runs on the host first: none of it
-        # depends on GPU results (the mock-model tokens are known).  (B) the phase's per-step
-        # metadata goes to the device in ONE copy and the decode kernels are launched back to back.
+        # Output phase, in two passes.  (A) every tree op of the phase — the slots of each step
+        # (R23: per step, in batch order), finished requests' dec_ref + insert — runs on the host
+        # first: none of it depends on GPU results (the mock-model tokens are known).  (B) the
+        # steps are launched: runs of single-token steps as decode calls with ONE metadata H2D,
+        # multi-token (jump-forward) steps as extend calls.
+        cur = n_prompt + first
         step = 0
         steps = []
         while len(running):
             t0 = time.perf_counter()
-            new = self._alloc(len(running))
-            pos = n_prompt[running] + step
-            slots[running, pos] = new
-            steps.append((running, new, pos))
-            self.stats["decode_tokens"] += len(running)
-            if self.plan_only:
-                hs = np.array([rs[b].hashes[p_] for b, p_ in zip(running, pos)], dtype=np.uint64)
-                self.calls.append(CallPlan("decode", hs, {"B": len(running)}))
+            lens = np.array([rs[b].segs[step] for b in running], dtype=np.int64)
+            new = self._alloc(int(lens.sum()))
+            pos = cur[running].copy()
+            if (lens == 1).all():
+                slots[running, pos] = new
+                steps.append(("dec", running, new, pos))
+                if self.plan_only:
+                    hs = np.array([rs[b].hashes[p_] for b, p_ in zip(running, pos)], dtype=np.uint64)
+                    self.calls.append(CallPlan("decode", hs, {"B": len(running)}))
+            else:
+                o_ = 0
+                for b, p_, n_ in zip(running, pos, lens):
+                    slots[b, p_:p_ + n_] = new[o_:o_ + n_]
+                    o_ += n_
+                steps.append(("ext", running, pos, lens))
+                if self.plan_only:
+                    hs = np.concatenate([rs[b].hashes[p_:p_ + n_] for b, p_, n_ in zip(running, pos, lens)])
+                    self.calls.append(CallPlan("extend", hs.astype(np.uint64), {"ext": lens.tolist()}))
+            cur[running] += lens
+            self.stats["decode_tokens"] += int(lens.sum())
             step += 1
-            done = n_out[running] <= step
+            done = nseg[running] <= step
             if done.any():
                 self._finish_many(rs, running[done], slots)
             running = running[~done]
             self.stats["tree_s"] += time.perf_counter() - t0
         if steps and not self.plan_only:
-            self._decode_phase(steps)
+            i = 0
+            while i < len(steps):
+                if steps[i][0] == "ext":
+                    _, running, pos, lens = steps[i]
+                    self._extend_step(rs, slots, running, pos, lens)
+                    i += 1
+                    continue
+                j = i
+                while j < len(steps) and steps[j][0] == "dec":
+                    j += 1
+                self._decode_phase([st[1:] for st in steps[i:j]])
+                i = j
         self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
         return rs
 
@@ -329,31 +424,48 @@ class Engine:
         B = len(rs)
         self.stats["extend_tokens"] += total
         if self.plan_only:
-            hs = np.array([h for r in rs for h in r.hashes[r.prefix:r.n_prompt]], dtype=np.uint64)
+            hs = np.array([h for r, n in zip(rs, ext) for h in r.hashes[r.prefix:r.prefix + n]], dtype=np.uint64)
             self.calls.append(CallPlan("extend", hs, {"ext": ext.tolist(), "prefix": prefix.tolist()}))
             return
+        self._extend_launch(slots, None, prefix, ext)
+
+    def _extend_step(self, rs, slots, running, pos, lens):
+        """A multi-token output step (jump forward): the running requests' segments
+        (sampled token + forced edge) are processed by one extend call over their cached context
+        (prefix = current length), table rows selected by `running`."""
+        self._extend_launch(slots, running, pos, lens)
+
+    def _extend_launch(self, slots, rows, prefix, ext):
+        """rx_extend over table `slots` (every row of the batch, uploaded whole so later decode
+        steps index it by batch row); batch entry b uses row rows[b] (None = identity)."""
         dev = self.device
+        B = len(prefix)
+        total = int(ext.sum())
         q, k_new, v_new = self.bank.ext[self._ext_i]
         self._ext_i += 1
-        # one pinned staging block: [prefix | ext | qo_indptr] then the rtt rows
-        stride = slots.shape[1]
-        hdr = 3 * (B + 1)
-        stage = self._pinned("ext", hdr + B * stride)
+        # one pinned staging block: [prefix | ext | qo_indptr | rows] then the rtt rows
+        R, stride = slots.shape
+        hdr = 4 * (B + 1)
+        stage = self._pinned("ext", hdr + R * stride)
         sn = stage.numpy()
         sn[0:B] = prefix
         sn[B + 1:2 * B + 1] = ext
         sn[2 * B + 2] = 0
         sn[2 * B + 3:3 * B + 3] = np.cumsum(ext)
+        if rows is not None:
+            sn[3 * B + 3:4 * B + 3] = rows
         sn[hdr:] = slots.reshape(-1)
         dstage = stage.to(dev, non_blocking=True)
         self._pinned_done("ext")
-        self._rtt = dstage[hdr:].view(B, stride)
-        self._B = B
-        ws_n = api.rx_decode_workspace_bytes(self.cfg, B, stride)
-        self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
+        self._rtt = dstage[hdr:].view(R, stride)
+        self._B = R
+        ws_n = api.rx_decode_workspace_bytes(self.cfg, R, stride)
+        if self._ws is None or self._ws.numel() < ws_n:
+            self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         ev0 = self._tbeg()
-        api.rx_extend(self.cfg, self._rtt, None, dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
+        api.rx_extend(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
+                      dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
                       total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o)
         nl = api.rx_last_launch_count()
         self.stats["launches"] += nl
@@ -499,6 +611,8 @@ class Engine:
         for kind, reqs in wl.phases:
             if kind == "queue":
                 self.run_waves(reqs)
+            elif kind == "fsm":
+                self.run_fsm_batch(reqs)
             else:
                 self.run_batch(reqs)
         return self

@@ -15,10 +15,10 @@ Both sides (``oracle/`` and ``paper_2312_07104_b200``) import this package;
 neither imports the other.
 """
 from .hashing import (GOLDEN, MASK64, splitmix64_int, splitmix64_np,
-                      splitmix64_t, prefix_hashes, next_token, sched_keys)
+                      splitmix64_t, prefix_hashes, next_token, sched_keys, fsm_choice)
 from .values import gen_values, gen_values_np
 
 __all__ = [
     "GOLDEN", "MASK64", "splitmix64_int", "splitmix64_np", "splitmix64_t",
-    "prefix_hashes", "next_token", "sched_keys", "gen_values", "gen_values_np",
+    "prefix_hashes", "next_token", "sched_keys", "fsm_choice", "gen_values", "gen_values_np",
 ]

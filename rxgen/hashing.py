@@ -81,3 +81,13 @@ def sched_keys(seed: int, wave: int, n: int) -> np.ndarray:
     splitmix64(seed ^ (wave << 32) ^ i).  An input, drawn identically for the oracle and the library."""
     x = np.arange(n, dtype=np.uint64) ^ np.uint64((int(seed) ^ (int(wave) << 32)) & MASK64)
     return splitmix64_np(x)
+
+
+FSM_SALT = 0xBB67AE8584CAA73B
+
+
+def fsm_choice(h: int, n: int) -> int:
+    """Mock model under a regex constraint (reading R28): after a prefix with hash h, pick option
+    splitmix64(h ^ FSM_SALT) mod n of the n allowed options (allowed bytes ascending, then STOP if
+    the state is accepting)."""
+    return splitmix64_int((int(h) ^ FSM_SALT) & MASK64) % n

@@ -161,4 +161,30 @@ def mix(seed: int = 0, groups: int = 4, per_group: int = 16, prefix: int = 1024,
                     {"groups": groups, "prefix": prefix})
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "MIX": mix}
+# character-profile JSON schema (cf. the paper's JSON example P:106-108): long constant
+# keys (jump-forward edges) between short free fields
+JSON_REGEX = (r'\{"name": "[A-Z][a-z]{2,9}", "age": [1-9]\d?, "occupation": "(engineer|doctor|teacher|artist)", '
+              r'"city": "[A-Z][a-z]{3,9}", "skills": \["[a-z]{3,8}", "[a-z]{3,8}", "[a-z]{3,8}"\], '
+              r'"summary": "[a-z ]{20,60}"\}')
+
+
+def json_decode(seed: int = 0, n_req: int = 64, prefix: int = 512, doc_lo: int = 64, doc_hi: int = 192,
+                compressed: bool = True, regex: str = JSON_REGEX, num_slots: int = 65536) -> Workload:
+    """JSON decoding under a regex ("JSON decoding with a schema specified by a regular
+    expression"): n_req requests share a `prefix`-token instruction
+    (sent first as a hint) plus a U[doc_lo, doc_hi] document each, and generate one JSON
+    object constrained by `regex` with a byte-level vocabulary (R26).  compressed=True decodes with
+    the compressed FSM (jump forward: a forced edge rides with the preceding token in one extend
+    pass), False token by token.  Llama-2-7B attention shape (32/32/128).  The output
+    lengths follow from the FSM walk of the mock model (R28); max_new_tokens bounds them."""
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    pre = _rand_tokens(rng, prefix, vocab)
+    reqs = [Request(np.concatenate([pre, _rand_tokens(rng, int(rng.integers(doc_lo, doc_hi + 1)), vocab)]), 512,
+                    f"j{i}") for i in range(n_req)]
+    return Workload("JSON", Shape(32, 32, 128), num_slots, vocab, seed,
+                    [("hint", [Request(pre, 0, "instr")]), ("fsm", reqs)],
+                    {"regex": regex, "compressed": compressed, "prefix": prefix})
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "MIX": mix, "JSON": json_decode}

@@ -144,3 +144,17 @@ def test_mix_schedule_parity(policy):
     oe = _compare(e, wl, _all_ext, _all_dec, policy=policy)
     assert oe.trace == e.trace
     assert any(t[0] == "evict" for t in e.trace)
+
+
+@pytest.mark.parametrize("compressed", [True, False])
+def test_json_fsm_parity(compressed):
+    """Regex-constrained JSON decoding (§4): compressed FSM (jump-forward segments as extend calls
+    with ragged 1..k-token rows over each request's cached context) and token-by-token decoding;
+    tree trace bit-exact, every attention row within tolerance."""
+    wl = workloads.json_decode(n_req=6, prefix=200, doc_lo=10, doc_hi=60, compressed=compressed, num_slots=8192)
+    e = _run_gpu(wl)
+    rows = lambda c, seqs: [(i, j) for i in range(len(seqs)) for j in range(400)]
+    oe = _compare(e, wl, rows, _all_dec)
+    assert oe.trace == e.trace
+    n_ext = sum(1 for x in e.outputs if x[0] == "extend")
+    assert (n_ext > 2) == compressed
