@@ -248,7 +248,22 @@ def main():
         achieved = kwork / kcalls / (per_launch_ms / 1000.0) / 1e9
         peak = peaks["hbm_gbs"]
         roof = {"bound": "hbm", "unit": "GB/s", "kernel": f"rx_{kind}"}
-    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+    # traffic: DRAM bytes per launch from the committed `ncu --set full` capture of this kernel in
+    # this workload (profiles/r1_ncu_<kind>_traffic_<wl>.json, scripts/ncu_traffic.py), expressed for
+    # this run's average launch: (captured DRAM bytes / captured algorithmic bytes) x algorithmic
+    # bytes per launch here
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", f"r1_ncu_{kind}_traffic_{wl.name}.json")
+    if os.path.exists(tp) and world == 1:
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = tj["traffic_over_algorithmic"] * (kwork / kcalls)
+        traffic_src = {"file": os.path.relpath(tp, ROOT), "captured_launches": len(tj["launches"]),
+                       "dram_bytes_per_captured_launch": tj["dram_bytes_per_launch"],
+                       "algorithmic_bytes_per_captured_launch": tj["algorithmic_bytes_per_launch"],
+                       "ratio": tj["traffic_over_algorithmic"]}
+    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
+                 "traffic_source": traffic_src,
                  "peak_source": f"{peak_src} MEASURED_PEAKS.json" if peak_src == "measured" else "fallback",
                  "share_of_step": kms / total_ms if world == 1 else None})
     kernels = {k_: {"ms_per_step": v_[0] / args.steps, "calls_per_step": v_[2] // args.steps,

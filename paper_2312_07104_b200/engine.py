@@ -123,7 +123,7 @@ class Engine:
         self.calls = []                      # CallPlan per attention call (plan pass)
         self.outputs = []                    # (kind, o tensor, meta) per call if keep_outputs
         self.stats = {"prompt_tokens": 0, "cached_prompt_tokens": 0, "extend_tokens": 0, "decode_tokens": 0,
-                      "tree_s": 0.0, "launches": 0}
+                      "output_tokens": 0, "tree_s": 0.0, "launches": 0}
         self._ext_i = 0
         self._dec_i = 0
         self.bank = None
@@ -139,6 +139,9 @@ class Engine:
         self._shared = 0
         self._ws = None
         self._fsm = None                      # compressed FSM of the workload's regex (JSON workload)
+        self.on_decode_plan = None            # callable(engine, slots, running, pos) per planned decode step
+        self.launch_chunk = 32                # output steps planned on the host per launch batch
+        self._ring = 0                        # rotating pinned staging buffers for decode metadata
         if not plan_only:
             hd = wl.shape.head_dim
             self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
@@ -326,6 +329,7 @@ class Engine:
             slots[b, :r.prefix] = r.slots
         self.stats["prompt_tokens"] += int(n_prompt.sum())
         self.stats["cached_prompt_tokens"] += int(prefix.sum())
+        self.stats["output_tokens"] += int(n_out.sum())
         ext = n_prompt + first - prefix
         new = self._alloc(int(ext.sum()))
         off = 0
@@ -350,11 +354,12 @@ class Engine:
         self._finish_many(rs, np.nonzero(nseg == 0)[0], slots)
         running = np.nonzero(nseg > 0)[0]
         self.stats["tree_s"] += time.perf_counter() - t0
-        # Output phase, in two passes.  (A) every tree op of the phase — the slots of each step
-        # (R23: per step, in batch order), finished requests' dec_ref + insert — runs on the host
-        # first: none of it depends on GPU results (the mock-model tokens are known).  (B) the
-        # steps are launched: runs of single-token steps as decode calls with ONE metadata H2D,
-        # multi-token (jump-forward) steps as extend calls.
+        # Output phase, host ahead of the device.  (A) the tree ops of each step — its slots (R23:
+        # per step, in batch order), finished requests' dec_ref + insert — run on the host: none of
+        # it depends on GPU results (the mock-model tokens are known).  (B) every launch_chunk
+        # steps the planned steps are launched: runs of single-token steps as decode calls with ONE
+        # metadata H2D, multi-token (jump-forward) steps as extend calls — so the GPU starts on
+        # the phase while the host plans the rest of it.
         cur = n_prompt + first
         step = 0
         steps = []
@@ -366,6 +371,8 @@ class Engine:
             if (lens == 1).all():
                 slots[running, pos] = new
                 steps.append(("dec", running, new, pos))
+                if self.on_decode_plan is not None:
+                    self.on_decode_plan(self, slots, running, pos)
                 if self.plan_only:
                     hs = np.array([rs[b].hashes[p_] for b, p_ in zip(running, pos)], dtype=np.uint64)
                     self.calls.append(CallPlan("decode", hs, {"B": len(running)}))
@@ -386,21 +393,28 @@ class Engine:
                 self._finish_many(rs, running[done], slots)
             running = running[~done]
             self.stats["tree_s"] += time.perf_counter() - t0
+            if len(steps) >= self.launch_chunk and not self.plan_only:
+                self._launch_steps(rs, slots, steps)          # keep the GPU fed while the host plans on
+                steps = []
         if steps and not self.plan_only:
-            i = 0
-            while i < len(steps):
-                if steps[i][0] == "ext":
-                    _, running, pos, lens = steps[i]
-                    self._extend_step(rs, slots, running, pos, lens)
-                    i += 1
-                    continue
-                j = i
-                while j < len(steps) and steps[j][0] == "dec":
-                    j += 1
-                self._decode_phase([st[1:] for st in steps[i:j]])
-                i = j
+            self._launch_steps(rs, slots, steps)
         self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
         return rs
+
+    def _launch_steps(self, rs, slots, steps):
+        """Launch planned output steps in order: runs of decode steps share one metadata H2D."""
+        i = 0
+        while i < len(steps):
+            if steps[i][0] == "ext":
+                _, running, pos, lens = steps[i]
+                self._extend_step(rs, slots, running, pos, lens)
+                i += 1
+                continue
+            j = i
+            while j < len(steps) and steps[j][0] == "dec":
+                j += 1
+            self._decode_phase([st[1:] for st in steps[i:j]])
+            i = j
 
     def _finish_many(self, rs, idx, slots):
         """Alg. 1 finished requests: dec_ref then insert(prompt + outputs), in batch order,
@@ -487,7 +501,9 @@ class Engine:
         dev = self.device
         offs = np.zeros(len(steps) + 1, dtype=np.int64)
         offs[1:] = np.cumsum([3 * len(r) for r, _, _ in steps])
-        stage = self._pinned("dec", int(offs[-1]))
+        name = f"dec{self._ring % 4}"
+        self._ring += 1
+        stage = self._pinned(name, int(offs[-1]))
         sn = stage.numpy()
         need = 0
         sh = self._shared
@@ -500,7 +516,7 @@ class Engine:
             need = max(need, api.rx_decode_cascade_workspace_bytes(self.cfg, B, ms, sh) if sh
                        else api.rx_decode_workspace_bytes(self.cfg, B, ms))
         d_all = stage.to(dev, non_blocking=True)
-        self._pinned_done("dec")
+        self._pinned_done(name)
         if need > self._ws.numel():
             self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
         for (running, new, pos), o0 in zip(steps, offs):
@@ -595,7 +611,8 @@ class Engine:
         self.trace = []
         self.outputs = []
         self._ext_i = self._dec_i = 0
-        for k in ("prompt_tokens", "cached_prompt_tokens", "extend_tokens", "decode_tokens", "launches"):
+        for k in ("prompt_tokens", "cached_prompt_tokens", "extend_tokens", "decode_tokens", "output_tokens",
+                  "launches"):
             self.stats[k] = 0
         self.stats["tree_s"] = 0.0
 

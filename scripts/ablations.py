@@ -47,9 +47,9 @@ def _time(wl, dev, flush, steps, warmup, policy="lspf"):
     st = plan.stats
     ms = sorted(ts)[len(ts) // 2]
     return {"hit_rate": st["cached_prompt_tokens"] / st["prompt_tokens"],
-            "extend_tokens": st["extend_tokens"], "output_tokens": st["decode_tokens"],
+            "extend_tokens": st["extend_tokens"], "output_tokens": st["output_tokens"],
             "passes": len(plan.calls), "extend_calls": sum(1 for c in plan.calls if c.kind == "extend"),
-            "ms_per_pass": ms, "served_tokens_per_s": (st["prompt_tokens"] + st["decode_tokens"]) / (ms / 1000.0)}
+            "ms_per_pass": ms, "served_tokens_per_s": (st["prompt_tokens"] + st["output_tokens"]) / (ms / 1000.0)}
 
 
 def main():
