@@ -274,41 +274,17 @@ def main():
     # ---------------------------------------------------------- e2e: host inputs, host outputs
     e2e = None
     if not args.no_e2e:
-        hbank = type(bank).__new__(type(bank))
-        hbank.ext = [tuple(t.cpu().pin_memory() for t in tr) for tr in bank.ext]
-        hbank.dec = [tuple(t.cpu().pin_memory() for t in tr) for tr in bank.dec]
-        h2d = sum(t.numel() * t.element_size() for lst in (hbank.ext, hbank.dec) for tr in lst for t in tr)
-
-        class DevBank:
-            """Moves each call's inputs host->device right before the call (inside the timed region)."""
-            def __init__(self, hb):
-                self.ext = _Lazy(hb.ext)
-                self.dec = _Lazy(hb.dec)
-
-        class _Lazy:
-            def __init__(self, lst):
-                self.lst = lst
-
-            def __getitem__(self, i):
-                return tuple(t.to(dev, non_blocking=True) for t in self.lst[i])
-
+        from paper_2312_07104_b200.hostio import HostInputs, HostSink
+        # every call's inputs live in pinned host memory and go host->device on a copy stream a few
+        # calls ahead; every call's output lands in a preallocated pinned host buffer via a D2H
+        # stream right after the call (paper_2312_07104_b200/hostio.py); sizes come from the plan
+        hbank = HostInputs(bank, dev)
+        h2d = hbank.h2d_bytes
         eng.enable_timing(False)
-        # every call's output lands in a preallocated pinned host buffer (D2H right after the call,
-        # overlapping the following work); sizes come from the plan
-        out_host = []
-        for c in plan.calls:
-            rows = len(c.hashes)
-            hq = eng.hq * world
-            out_host.append(torch.empty((rows, hq, wl.shape.head_dim), dtype=torch.bfloat16, pin_memory=True))
-        d2h = [sum(t.numel() * t.element_size() for t in out_host)]
-        slot = [0]
-
-        def sink(kind, o):
-            dst = out_host[slot[0]]
-            dst.view(o.shape).copy_(o, non_blocking=True) if o.is_contiguous() else dst.copy_(o.reshape(dst.shape),
-                                                                                               non_blocking=True)
-            slot[0] += 1
-
+        hq = eng.hq * world
+        sink = HostSink([torch.empty((len(c.hashes), hq, wl.shape.head_dim), dtype=torch.bfloat16, pin_memory=True)
+                         for c in plan.calls], dev)
+        d2h = [sink.d2h_bytes]
         eng.sink = sink
         e2e_times = []
         for it in range(max(1, args.steps)):
@@ -317,10 +293,12 @@ def main():
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
-            slot[0] = 0
+            sink.reset()
             a.record()
+            hbank.reset()
             eng.reset()
-            eng.run_workload(DevBank(hbank))
+            eng.run_workload(hbank)
+            sink.join()
             b.record()
             torch.cuda.synchronize()
             e2e_times.append(a.elapsed_time(b))

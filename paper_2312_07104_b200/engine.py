@@ -24,6 +24,7 @@ reassembled by one all_gather per attention call (see ``tp.py``).
 """
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -140,7 +141,7 @@ class Engine:
         self._ws = None
         self._fsm = None                      # compressed FSM of the workload's regex (JSON workload)
         self.on_decode_plan = None            # callable(engine, slots, running, pos) per planned decode step
-        self.launch_chunk = 32                # output steps planned on the host per launch batch
+        self.launch_chunk = int(os.environ.get("RX_LAUNCH_CHUNK", "32"))   # output steps planned per launch batch
         self._ring = 0                        # rotating pinned staging buffers for decode metadata
         if not plan_only:
             hd = wl.shape.head_dim
@@ -518,7 +519,7 @@ class Engine:
         d_all = stage.to(dev, non_blocking=True)
         self._pinned_done(name)
         if need > self._ws.numel():
-            self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
+            self._ws = torch.empty(2 * need, dtype=torch.uint8, device=dev)   # geometric growth
         for (running, new, pos), o0 in zip(steps, offs):
             B = len(running)
             q, k, v = self.bank.dec[self._dec_i]
