@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../../include/rx.h"
 
@@ -18,6 +19,18 @@ rx_status check_cfg(const rx_attn_cfg* c) {
   if (!(c->head_dim == 64 || c->head_dim == 128)) return RX_E_UNSUPPORTED;
   if (!(G == 1 || G == 2 || G == 4 || G == 8)) return RX_E_UNSUPPORTED;
   return RX_OK;
+}
+// rx_extend kernel choice: the multi-query decode kernel when every request's segment is at most
+// 32 (row, head) columns (<= 4 column tiles of 8) and (request, kv head) pairs alone fill the SMs
+// (it runs one split per request); the tcgen05 extend kernel otherwise.  RX_EXTEND_MULTI=0 turns
+// the multi-query path off (A/B knob).
+bool use_multi_query(int G, int batch, int h_kv, int max_ext) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("RX_EXTEND_MULTI");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0 && max_ext * G <= 32 && int64_t(batch) * h_kv >= 148;
 }
 }  // namespace
 
@@ -259,7 +272,30 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
                                           d_prefix_lens, d_rows, d_rtt, rtt_stride, d_k_new, d_v_new, d_k_pool,
                                           d_v_pool, st);
   if (e != cudaSuccess) return RX_E_CUDA;
-  e = rx::launch_extend(cfg->head_dim, cfg->h_q / cfg->h_kv, p, d_q, total_new, batch, max_extend_len, st);
+  const int G = cfg->h_q / cfg->h_kv;
+  if (use_multi_query(G, batch, cfg->h_kv, max_extend_len)) {
+    // short segments (jump-forward edges, §4): (row, head) columns of the decode kernel's
+    // mma.sync tile instead of 128-row tcgen05 tiles that would be almost all padding
+    rx::DecodeParams dp{};
+    dp.q = static_cast<const __nv_bfloat16*>(d_q);
+    dp.kpool = static_cast<const __nv_bfloat16*>(d_k_pool);
+    dp.vpool = static_cast<const __nv_bfloat16*>(d_v_pool);
+    dp.o = static_cast<__nv_bfloat16*>(d_o);
+    dp.rtt = d_rtt;
+    dp.rtt_stride = rtt_stride;
+    dp.rows = d_rows;
+    dp.h_q = cfg->h_q;
+    dp.h_kv = cfg->h_kv;
+    dp.chunk = (max_prefix_len + max_extend_len + 15) / 16 * 16;   // one split per request
+    dp.max_splits = 1;
+    dp.scale_log2 = p.scale_log2;
+    dp.qo_indptr = d_qo_indptr;
+    dp.prefix_lens = d_prefix_lens;
+    dp.col_tiles = (max_extend_len * G + 7) / 8;
+    e = rx::launch_decode_multi(cfg->head_dim, G, dp, batch, st);
+  } else {
+    e = rx::launch_extend(cfg->head_dim, G, p, d_q, total_new, batch, max_extend_len, st);
+  }
   if (e != cudaSuccess) return RX_E_CUDA;
   g_last_launches = 2;
   return RX_OK;

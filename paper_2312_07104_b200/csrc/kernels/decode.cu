@@ -18,6 +18,10 @@
 //  * warps merge through shared memory; splits merge by log-sum-exp in a
 //    second small kernel (A8), or the CTA writes bf16 output directly when
 //    the request has a single split.
+//  * MULTI = true: the same kernel for short extends (a jump-forward segment of
+//    a few tokens, §4): the 8 MMA columns are (query row j, GQA head h)
+//    pairs of one request, each with its own causal limit; one split per
+//    request.  Used by rx_extend when every segment fits a few column tiles.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -62,12 +66,17 @@ __device__ __forceinline__ void dec_issue_block(uint32_t kdst, uint32_t vdst, co
   }
 }
 
-template <int HD, int G, int STAGES>
+template <int HD, int G, int STAGES, bool MULTI = false>
 __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeParams p) {
   using C = DecCfg<HD, STAGES>;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int b = blockIdx.z, g = blockIdx.y, s = blockIdx.x;
-  const int L = p.seq_lens[b];
+  const int b = MULTI ? int(blockIdx.z) / p.col_tiles : int(blockIdx.z), g = blockIdx.y, s = blockIdx.x;
+  // MULTI: this CTA's columns are ct*8 .. ct*8+7 of the request's nq*G (row, head) pairs
+  const int ct = MULTI ? int(blockIdx.z) % p.col_tiles : 0;
+  const int q0 = MULTI ? p.qo_indptr[b] : b;
+  const int nq = MULTI ? p.qo_indptr[b + 1] - q0 : 1;
+  if (MULTI && ct * 8 >= nq * G) return;
+  const int L = MULTI ? p.prefix_lens[b] + nq : p.seq_lens[b];
   const int start = p.kv_start + s * p.chunk;      // kv_start > 0: cascade (shared prefix elsewhere)
   if (start >= L) return;
   const int end = min(L, start + p.chunk);
@@ -80,7 +89,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   // into the pool slot (A5) and, for kv head 0, appends the slot to the
   // req_to_token row (A4); position L-1 then reads its slot from the argument,
   // never from the table, so no CTA races the table write.
-  const bool append = p.new_slots != nullptr;
+  const bool append = !MULTI && p.new_slots != nullptr;
   const int new_slot = append ? p.new_slots[b] : 0;
   if (append && s == nsplit - 1) {
     constexpr int VPR = HD / 8;                      // 16-byte vectors per head row
@@ -102,10 +111,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   // Q^T fragments (B operand): b0 = Q[head gq][16kk + 2tq .. +1], b1 = Q[head gq][16kk + 8 + 2tq .. +1]
   uint32_t qf[HD / 16][2];
   {
-    const __nv_bfloat16* qrow = p.q + (int64_t(b) * p.h_q + g * G + gq) * HD;
+    // column gq: decode -> head gq of the group (padded past G); MULTI -> row j, head h
+    const int cj = MULTI ? (ct * 8 + gq) / G : 0, ch = MULTI ? (ct * 8 + gq) % G : gq;
+    const bool qok = MULTI ? cj < nq : gq < G;
+    const __nv_bfloat16* qrow = p.q + (int64_t(q0 + (qok ? cj : 0)) * p.h_q + g * G + (qok ? ch : 0)) * HD;
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      if (gq < G) {
+      if (qok) {
         qf[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tq);
         qf[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tq);
       } else {
@@ -165,11 +177,18 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
         mma_bf16_16816(sacc, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
       }
     }
-    // scale into log2 domain; mask tokens past the end of the split
-    float s0 = gq < nvalid ? sacc[0] * p.scale_log2 : -INFINITY;
-    float s1 = gq < nvalid ? sacc[1] * p.scale_log2 : -INFINITY;
-    float s2 = gq + 8 < nvalid ? sacc[2] * p.scale_log2 : -INFINITY;
-    float s3 = gq + 8 < nvalid ? sacc[3] * p.scale_log2 : -INFINITY;
+    // scale into log2 domain; mask tokens past the end of the split (MULTI: and past each
+    // column's own position, causal inside the segment)
+    int lim0 = nvalid, lim1 = nvalid;
+    if (MULTI) {
+      const int base = L - nq - tok0(i);             // position of the segment's first row, block-relative
+      lim0 = min(nvalid, base + (ct * 8 + 2 * tq) / G + 1);
+      lim1 = min(nvalid, base + (ct * 8 + 2 * tq + 1) / G + 1);
+    }
+    float s0 = gq < lim0 ? sacc[0] * p.scale_log2 : -INFINITY;
+    float s1 = gq < lim1 ? sacc[1] * p.scale_log2 : -INFINITY;
+    float s2 = gq + 8 < lim0 ? sacc[2] * p.scale_log2 : -INFINITY;
+    float s3 = gq + 8 < lim1 ? sacc[3] * p.scale_log2 : -INFINITY;
     float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -177,11 +196,15 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
     }
     const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float c0 = fast_exp2(m0 - mn0), c1 = fast_exp2(m1 - mn1);
+    // MULTI: a column may meet a fully masked block before any valid key (its running max stays
+    // -inf); exponentiate against 0 then, so every factor is 0 instead of NaN
+    const float e0 = (MULTI && mn0 == -INFINITY) ? 0.f : mn0;
+    const float e1 = (MULTI && mn1 == -INFINITY) ? 0.f : mn1;
+    const float c0 = fast_exp2(m0 - e0), c1 = fast_exp2(m1 - e1);
     m0 = mn0;
     m1 = mn1;
-    const float p0 = fast_exp2(s0 - mn0), p1 = fast_exp2(s1 - mn1);
-    const float p2 = fast_exp2(s2 - mn0), p3 = fast_exp2(s3 - mn1);
+    const float p0 = fast_exp2(s0 - e0), p1 = fast_exp2(s1 - e1);
+    const float p2 = fast_exp2(s2 - e0), p3 = fast_exp2(s3 - e1);
     l0 = l0 * c0 + p0 + p2;
     l1 = l1 * c1 + p1 + p3;
 #pragma unroll
@@ -232,8 +255,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
     ow[(d + 8) * 8 + 2 * tq + 1] = oacc[mt][3];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < G * HD; idx += kDecWarps * 32) {
-    const int h = idx / HD, d = idx % HD;
+  for (int idx = threadIdx.x; idx < (MULTI ? 8 : G) * HD; idx += kDecWarps * 32) {
+    const int h = idx / HD, d = idx % HD;   // MULTI: h is the column
+    if (MULTI && (ct * 8 + h) / G >= nq) continue;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, red_m[w][h]);
@@ -243,6 +267,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
       const float f = fast_exp2(red_m[w][h] - M);
       Ls += f * red_l[w][h];
       acc += f * opart[(w * HD + d) * 8 + h];
+    }
+    if (MULTI) {   // one split: every column saw key 0, so Ls > 0
+      const int j = (ct * 8 + h) / G, hq = g * G + (ct * 8 + h) % G;
+      p.o[(int64_t(q0 + j) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / Ls);
+      continue;
     }
     const int hq = g * G + h;
     if (nsplit == 1 && p.split_base == 0) {
@@ -290,6 +319,29 @@ static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_
     *launches = 2;
   }
   return cudaPeekAtLastError();
+}
+
+template <int HD, int G>
+static cudaError_t launch_decode_multi_t(const DecodeParams& p, int batch, cudaStream_t st) {
+  constexpr int STG = HD == 64 ? 6 : 2;
+  using C = DecCfg<HD, STG>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_kernel<HD, G, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  dim3 grid(1, p.h_kv, batch * p.col_tiles);
+  decode_kernel<HD, G, STG, true><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);
+  return cudaPeekAtLastError();
+}
+
+cudaError_t launch_decode_multi(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st) {
+#define RX_DEC_CASE(HD_, G_) \
+  if (head_dim == HD_ && G == G_) return launch_decode_multi_t<HD_, G_>(p, batch, st);
+  RX_DEC_CASE(64, 1) RX_DEC_CASE(64, 2) RX_DEC_CASE(64, 4) RX_DEC_CASE(64, 8)
+  RX_DEC_CASE(128, 1) RX_DEC_CASE(128, 2) RX_DEC_CASE(128, 4) RX_DEC_CASE(128, 8)
+#undef RX_DEC_CASE
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st) {

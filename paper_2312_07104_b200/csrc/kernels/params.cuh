@@ -37,6 +37,13 @@ struct DecodeParams {
   // the split_base shared partials); the merge combines split_base + nsplit_b.
   int kv_start;
   int split_base;
+  // multi-query mode (rx_extend with short segments, decode_kernel<..., MULTI>): request b owns
+  // query rows qo_indptr[b] .. qo_indptr[b+1] (q / o ragged [N, h_q, HD]) at positions
+  // prefix_lens[b] + j; causal inside the segment; CTA z = b * col_tiles + tile of 8 columns
+  // (column = row j x GQA head); one split per request (chunk >= every sequence)
+  const int32_t* qo_indptr;
+  const int32_t* prefix_lens;
+  int col_tiles;
 };
 
 struct ExtendParams {
@@ -141,6 +148,7 @@ cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, 
 cudaError_t launch_extend_cascade(int head_dim, int G, const ExtendParams& p, const void* q, int batch,
                                   cudaStream_t st);
 cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st, int* launches);
+cudaError_t launch_decode_multi(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st);
 cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void* q, int64_t total_new, int batch,
                           int max_ext, cudaStream_t st);
 

@@ -142,7 +142,9 @@ class Engine:
         self._fsm = None                      # compressed FSM of the workload's regex (JSON workload)
         self.on_decode_plan = None            # callable(engine, slots, running, pos) per planned decode step
         self.launch_chunk = int(os.environ.get("RX_LAUNCH_CHUNK", "32"))   # output steps planned per launch batch
+        self.gather_chunk_rows = 8192         # TP: extend rows per overlapped all-gather block
         self._ring = 0                        # rotating pinned staging buffers for decode metadata
+        self._ext_ring = 0                    # ... and for extend metadata + tables
         if not plan_only:
             hd = wl.shape.head_dim
             self.k_pool = torch.zeros((wl.num_slots, self.hkv, hd), dtype=torch.bfloat16, device=device)
@@ -461,7 +463,9 @@ class Engine:
         # one pinned staging block: [prefix | ext | qo_indptr | rows] then the rtt rows
         R, stride = slots.shape
         hdr = 4 * (B + 1)
-        stage = self._pinned("ext", hdr + R * stride)
+        name = f"ext{self._ext_ring % 8}"            # ring: the host may run several extends ahead
+        self._ext_ring += 1
+        stage = self._pinned(name, hdr + R * stride)
         sn = stage.numpy()
         sn[0:B] = prefix
         sn[B + 1:2 * B + 1] = ext
@@ -471,30 +475,78 @@ class Engine:
             sn[3 * B + 3:4 * B + 3] = rows
         sn[hdr:] = slots.reshape(-1)
         dstage = stage.to(dev, non_blocking=True)
-        self._pinned_done("ext")
+        self._pinned_done(name)
         self._rtt = dstage[hdr:].view(R, stride)
         self._B = R
         ws_n = api.rx_decode_workspace_bytes(self.cfg, R, stride)
         if self._ws is None or self._ws.numel() < ws_n:
             self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+        chunks = self._gather_chunks(ext) if (self.gather is not None and hasattr(self.gather, "start")) else None
         ev0 = self._tbeg()
-        api.rx_extend(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
-                      dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
-                      total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o)
-        nl = api.rx_last_launch_count()
+        if chunks is None:
+            api.rx_extend(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
+                          dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
+                          total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o)
+            nl = api.rx_last_launch_count()
+        else:
+            # TP: the call runs as request blocks; each block's rows are all-gathered (async, NCCL
+            # stream) while the next block computes (SURVEY §8(e) chunked overlap)
+            nl = 0
+            out = self.gather.alloc(total, self.hq, self.shape.head_dim, o.dtype, dev)
+            handles = []
+            cname = f"extc{self._ext_ring % 8}"
+            cst = self._pinned(cname, 4 * (B + len(chunks)))
+            cn = cst.numpy()
+            o_ = 0
+            meta = []
+            for b0, b1 in chunks:
+                n = b1 - b0
+                cn[o_:o_ + n] = prefix[b0:b1]
+                cn[o_ + n:o_ + 2 * n] = ext[b0:b1]
+                cn[o_ + 2 * n] = 0
+                cn[o_ + 2 * n + 1:o_ + 3 * n + 1] = np.cumsum(ext[b0:b1])
+                cn[o_ + 3 * n + 1:o_ + 4 * n + 1] = rows[b0:b1] if rows is not None else np.arange(b0, b1)
+                meta.append((o_, n))
+                o_ += 4 * n + 1
+            dchunk = cst.to(dev, non_blocking=True)
+            self._pinned_done(cname)
+            qo = np.concatenate([[0], np.cumsum(ext)])
+            for (b0, b1), (c0, n) in zip(chunks, meta):
+                r0, r1 = int(qo[b0]), int(qo[b1])
+                if r1 == r0:
+                    continue
+                d = dchunk[c0:c0 + 4 * n + 1]
+                api.rx_extend(self.cfg, self._rtt, d[3 * n + 1:4 * n + 1], d[0:n], d[n:2 * n], d[2 * n:3 * n + 1],
+                              r1 - r0, int(ext[b0:b1].max()), int(prefix[b0:b1].max()), q[r0:r1], k_new[r0:r1],
+                              v_new[r0:r1], self.k_pool, self.v_pool, o[r0:r1])
+                nl += api.rx_last_launch_count()
+                handles.append(self.gather.start(o[r0:r1], out, r0, r1))
         self.stats["launches"] += nl
         if ev0 is not None:
             # algorithmic FLOPs: 4*hd*H_q*sum(n*p + n(n+1)/2), causal-masked work not counted
             n, p_ = ext.astype(np.float64), prefix.astype(np.float64)
             flops = 4.0 * self.shape.head_dim * self.hq * float(np.sum(n * p_ + n * (n + 1) / 2))
             self._tend(ev0, "extend", flops, nl)
-        if self.gather is not None:
+        if chunks is not None:
+            o = self.gather.finish(handles, out)
+        elif self.gather is not None:
             o = self.gather(o)
         if self.sink is not None:
             self.sink("extend", o)
         if self.keep_outputs:
             self.outputs.append(("extend", o, {"ext": ext.tolist()}))
+
+    def _gather_chunks(self, ext):
+        """Request blocks of a TP extend call whose outputs are gathered while later blocks run:
+        about gather_chunk_rows rows each; None when the call is small (one gather)."""
+        total = int(ext.sum())
+        if total < 2 * self.gather_chunk_rows:
+            return None
+        cum = np.cumsum(ext)
+        cuts = np.searchsorted(cum, np.arange(self.gather_chunk_rows, total, self.gather_chunk_rows), side="left") + 1
+        edges = [0] + sorted(set(int(c) for c in cuts if 0 < c < len(ext))) + [len(ext)]
+        return [(edges[i], edges[i + 1]) for i in range(len(edges) - 1)] if len(edges) > 2 else None
 
     def _decode_phase(self, steps):
         """Launch a batch's decode steps: one H2D of [new_slots | seq_lens | rows] for every step,

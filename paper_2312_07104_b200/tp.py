@@ -22,25 +22,49 @@ import torch
 import torch.distributed as dist
 
 
-def make_gather(group=None):
-    """Return gather(o_local [N, hq_local, hd]) -> o [N, P, hq_local, hd].
+class Gather:
+    """gather(o_local [N, hq_local, hd]) -> o [N, P, hq_local, hd].
 
     The result is a strided VIEW of the rank-major all-gather buffer [P, N,
     hq_local, hd]: global q head = rank * hq_local + local head.  No permute
-    copy is made (callers that need a dense [N, H_q, hd] reshape it)."""
-    world = dist.get_world_size(group)
-    use_tensor_api = dist.get_backend(group) == "nccl"
+    copy is made (callers that need a dense [N, H_q, hd] reshape it).
 
-    def gather(o_local: torch.Tensor) -> torch.Tensor:
+    Chunked form for large calls (a C5 suffix extend gathers
+    268 MB): ``alloc`` the buffer, ``start`` an asynchronous all-gather of
+    each finished row block while the next block computes (NCCL's stream waits
+    only for the work enqueued before the call), ``finish`` joins them."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.tensor_api = dist.get_backend(group) == "nccl"
+
+    def __call__(self, o_local: torch.Tensor) -> torch.Tensor:
         o_local = o_local.contiguous()
-        out = torch.empty((world,) + tuple(o_local.shape), dtype=o_local.dtype, device=o_local.device)
-        if use_tensor_api:
-            dist.all_gather_into_tensor(out, o_local, group=group)
+        out = torch.empty((self.world,) + tuple(o_local.shape), dtype=o_local.dtype, device=o_local.device)
+        if self.tensor_api:
+            dist.all_gather_into_tensor(out, o_local, group=self.group)
         else:
-            dist.all_gather(list(out.unbind(0)), o_local, group=group)
+            dist.all_gather(list(out.unbind(0)), o_local, group=self.group)
         return out.permute(1, 0, 2, 3)
 
-    return gather
+    def alloc(self, n, hq_local, hd, dtype, device):
+        return torch.empty((self.world, n, hq_local, hd), dtype=dtype, device=device)
+
+    def start(self, o_part: torch.Tensor, out: torch.Tensor, r0: int, r1: int):
+        """all-gather rows [r0, r1) of every rank into out[:, r0:r1] (async)."""
+        return dist.all_gather([out[r, r0:r1] for r in range(self.world)], o_part.contiguous(), group=self.group,
+                               async_op=True)
+
+    @staticmethod
+    def finish(handles, out):
+        for h in handles:
+            h.wait()
+        return out.permute(1, 0, 2, 3)
+
+
+def make_gather(group=None):
+    return Gather(group)
 
 
 def tree_digest(cache) -> str:

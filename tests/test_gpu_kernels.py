@@ -150,6 +150,25 @@ EXT_CASES = [
 ]
 
 
+def _short_segments(seed, B, max_ext, max_pre):
+    r = np.random.default_rng(seed)
+    pre = [int(x) for x in r.integers(0, max_pre + 1, B)]
+    ext = [int(x) for x in r.integers(0, max_ext + 1, B)]
+    pre[0], ext[0], ext[1] = 0, max_ext, 0          # no prefix; the widest segment; an empty one
+    return pre, ext
+
+
+# short segments with enough (request, kv head) pairs: rx_extend takes the multi-query decode
+# kernel (max_ext * G <= 32, batch * h_kv >= 148): jump-forward edges of constrained decoding
+EXT_CASES += [
+    (32, 32, 128, *_short_segments(1, 8, 20, 700), False),     # G=1: up to 3 column tiles
+    (32, 32, 128, *_short_segments(2, 6, 32, 300), True),      # 4 tiles
+    (32, 8, 128, *_short_segments(3, 20, 8, 900), False),      # G=4
+    (64, 8, 128, *_short_segments(4, 20, 4, 500), False),      # G=8
+    (8, 2, 64, *_short_segments(5, 80, 8, 200), False),        # hd 64
+]
+
+
 @pytest.mark.parametrize("h_q,h_kv,hd,pre,ext,contig", EXT_CASES)
 @pytest.mark.parametrize("q_scale", [1.0, 4.0])
 def test_extend_vs_oracle(h_q, h_kv, hd, pre, ext, contig, q_scale):

@@ -49,3 +49,34 @@ def test_fake_tp_matches_single_gpu(make, P):
         err = (o_tp.float() - o_full.float()).abs().max().item()
         worst = max(worst, err)
     assert worst <= 2e-2, worst
+
+
+def test_chunked_overlapped_gather_world1_nccl():
+    """The TP extend path with the output all-gather split into request blocks and overlapped with
+    the next block's compute (NCCL async, one-rank group on this GPU): outputs are bit-identical to
+    the unchunked call (blocks never split a request; each request's math is unchanged)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2312_07104_b200.tp import make_gather
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    wl = workloads.c5(n_req=12, prefix=600, question=40, decode=3, num_slots=16384, ragged=True)
+    ref = _run(wl)
+    _, bank = plan_and_bank(wl, "cuda")
+    e = Engine(wl, "cuda", record=True, keep_outputs=True, gather=make_gather())
+    e.gather_chunk_rows = 100                       # several blocks for the 12 x U[64,256]-row extend
+    assert e._gather_chunks(np.array([150] * 12)) is not None
+    e.run_workload(bank)
+    torch.cuda.synchronize()
+    assert e.trace == ref.trace
+    for (k1, o1, _), (k2, o2, _) in zip(ref.outputs, e.outputs):
+        assert k1 == k2
+        assert torch.equal(o1, o2.reshape(o1.shape))
+    dist.destroy_process_group()
