@@ -339,6 +339,12 @@ rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
  *   max_extend_len   = max extend_len (host copy, sizes the grid)
  *   max_prefix_len   = max prefix_len (host copy); rtt_stride must be >= every
  *       prefix_len + extend_len (only the maxima are checked)
+ * Kernel choice (same results within the attention tolerance): the tcgen05
+ * tile kernel, or — when max_extend_len * (h_q / h_kv) <= 32 and batch * h_kv
+ * >= 148, i.e. short segments such as jump-forward edges of constrained
+ * decoding (§4) — the decode kernel in multi-query mode (one mma.sync
+ * column per (row, GQA head), causal per column).  Two launches either way
+ * (store, attention).
  * Workspace: d_ws of ws_bytes >= rx_extend_workspace_bytes(...). */
 rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch,
                     const int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,

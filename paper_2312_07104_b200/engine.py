@@ -572,6 +572,12 @@ class Engine:
         self._pinned_done(name)
         if need > self._ws.numel():
             self._ws = torch.empty(2 * need, dtype=torch.uint8, device=dev)   # geometric growth
+        # timing: one event pair around the whole run of back-to-back decode calls (per-call events
+        # on ~2000 calls per C3 step would perturb the step); per call when outputs are gathered
+        # (TP), so the all-gather stays outside the kernel brackets
+        per_call = self.gather is not None
+        ev_run = None if per_call else self._tbeg()
+        works, nl_run = [], 0
         for (running, new, pos), o0 in zip(steps, offs):
             B = len(running)
             q, k, v = self.bank.dec[self._dec_i]
@@ -579,7 +585,7 @@ class Engine:
             d = d_all[o0:o0 + 3 * B]
             max_seq = int(pos.max()) + 1
             o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
-            ev0 = self._tbeg()
+            ev0 = self._tbeg() if per_call else None
             if sh:
                 api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, sh, q, k, v,
                                              d[:B], self.k_pool, self.v_pool, o, self._ws)
@@ -588,16 +594,20 @@ class Engine:
                                      self.k_pool, self.v_pool, o, self._ws)
             nl = api.rx_last_launch_count()
             self.stats["launches"] += nl
+            # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot indices,
+            # computed after the timed region from (slots, running, pos)
             if ev0 is not None:
-                # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot indices,
-                # computed after the timed region from (slots, running, pos)
-                self._tend(ev0, "decode", (self._slots_host, running, pos), nl)
+                self._tend(ev0, "decode", [(self._slots_host, running, pos)], nl)
+            works.append((self._slots_host, running, pos))
+            nl_run += nl
             if self.gather is not None:
                 o = self.gather(o)
             if self.sink is not None:
                 self.sink("decode", o)
             if self.keep_outputs:
                 self.outputs.append(("decode", o, {"B": B}))
+        if ev_run is not None:
+            self._tend(ev_run, "decode", works, nl_run, calls=len(steps))
 
     # ------------------------------------------------------------------ pinned staging
     def _pinned(self, name, n):
@@ -627,10 +637,10 @@ class Engine:
         e.record()
         return e
 
-    def _tend(self, ev0, kind, work, launches):
+    def _tend(self, ev0, kind, work, launches, calls=1):
         e = torch.cuda.Event(enable_timing=True)
         e.record()
-        self.timer.append((kind, ev0, e, work, launches))
+        self.timer.append((kind, ev0, e, work, launches, calls))
 
     def decode_bytes(self, work):
         """(algorithmic, logical) bytes of one rx_decode call: distinct pool rows read once (K+V),
@@ -647,13 +657,13 @@ class Engine:
     def timing_summary(self):
         """{kind: (total ms, launches, calls, total work)} from the recorded events (call after a sync)."""
         out = {}
-        for kind, a, b, work, nl in self.timer or []:
+        for kind, a, b, work, nl, calls in self.timer or []:
             ms = a.elapsed_time(b)
             t = out.setdefault(kind, [0.0, 0, 0, 0.0])
             t[0] += ms
             t[1] += nl
-            t[2] += 1
-            t[3] += self.decode_bytes(work)[0] if kind == "decode" else work
+            t[2] += calls
+            t[3] += sum(self.decode_bytes(w)[0] for w in work) if kind == "decode" else work
         return out
 
     # ------------------------------------------------------------------ workloads

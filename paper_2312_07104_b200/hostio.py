@@ -2,7 +2,7 @@
 
 A serving process receives each attention call's q / k_new / v_new from the host and returns its
 output to the host.  ``HostInputs`` keeps every call's inputs in pinned host memory and copies
-them host->device on a dedicated copy stream ``depth`` calls ahead of use (the compute stream waits
+them host->device on dedicated copy streams ``depth`` calls ahead of use (the compute stream waits
 on a per-call event); ``HostSink`` copies every output device->host on a second stream as soon as
 the call that produced it retires.  Both directions of PCIe run concurrently with the kernels, so
 an end-to-end step costs max(kernels, H2D, D2H) instead of their sum.  Plumbing only: no method
@@ -47,15 +47,76 @@ class _Prefetcher:
         return ts
 
 
+class _BlockPrefetcher:
+    """Like _Prefetcher for many small calls (decode steps): the calls' tensors live back to back in
+    ONE pinned byte buffer and are copied `block` calls per cudaMemcpy, `depth` blocks ahead, so
+    the host issues one copy per block instead of three per call."""
+
+    def __init__(self, host_list, device, block, depth, stream):
+        self.dev, self.block, self.depth, self.stream = device, block, depth, stream
+        self.meta = []                         # per call: [(byte offset, nbytes, dtype, shape)]
+        off = 0
+        for tr in host_list:
+            m = []
+            for t in tr:
+                nb = t.numel() * t.element_size()
+                m.append((off, nb, t.dtype, tuple(t.shape)))
+                off += (nb + 255) // 256 * 256
+            self.meta.append(m)
+        self.h2d_bytes = sum(t.numel() * t.element_size() for tr in host_list for t in tr)
+        self.buf = torch.empty(max(off, 1), dtype=torch.uint8, pin_memory=True)
+        for tr, m in zip(host_list, self.meta):
+            for t, (o, nb, _, _) in zip(tr, m):
+                self.buf[o:o + nb].copy_(t.reshape(-1).view(torch.uint8))
+        n = len(host_list)
+        self.ranges = []                       # per block: (first byte, end byte)
+        for b0 in range(0, n, block):
+            b1 = min(n, b0 + block)
+            first = self.meta[b0][0][0]
+            last = self.meta[b1 - 1][-1]
+            self.ranges.append((first, last[0] + last[1]))
+        self.pending = {}
+
+    def reset(self):
+        self.pending.clear()
+
+    def _issue(self, j):
+        if j >= len(self.ranges) or j in self.pending:
+            return
+        a, b = self.ranges[j]
+        with torch.cuda.stream(self.stream):
+            d = self.buf[a:b].to(self.dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self.pending[j] = (d, ev, a, False)
+
+    def __getitem__(self, i):
+        j = i // self.block
+        for k in range(j, j + self.depth):
+            self._issue(k)
+        d, ev, a, waited = self.pending[j]
+        cur = torch.cuda.current_stream()
+        if not waited:
+            cur.wait_event(ev)
+            d.record_stream(cur)
+            self.pending[j] = (d, ev, a, True)
+        out = tuple(d[o - a:o - a + nb].view(dt).view(shape) for o, nb, dt, shape in self.meta[i])
+        if i % self.block == self.block - 1 or i == len(self.meta) - 1:
+            self.pending.pop(j)
+        return out
+
+
 class HostInputs:
     """Drop-in for ``engine.InputBank`` with the tensors in pinned host memory."""
 
-    def __init__(self, bank, device, ext_depth=2, dec_depth=16):
-        self.stream = torch.cuda.Stream(device=device)
+    def __init__(self, bank, device, ext_depth=2, dec_block=16, dec_depth=4):
+        # one copy stream per call kind: a large extend prefetch (~1 GB for a C3 turn) must not
+        # queue in front of the small per-step decode inputs that are needed first
+        self.streams = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device))
         hext = [tuple(t.cpu().pin_memory() for t in tr) for tr in bank.ext]
         hdec = [tuple(t.cpu().pin_memory() for t in tr) for tr in bank.dec]
-        self.ext = _Prefetcher(hext, device, ext_depth, self.stream)
-        self.dec = _Prefetcher(hdec, device, dec_depth, self.stream)
+        self.ext = _Prefetcher(hext, device, ext_depth, self.streams[0])
+        self.dec = _BlockPrefetcher(hdec, device, dec_block, dec_depth, self.streams[1])
 
     @property
     def h2d_bytes(self):
@@ -65,7 +126,8 @@ class HostInputs:
         self.ext.reset()
         self.dec.reset()
         # nothing is copied before the caller's current stream reaches this point (timed regions)
-        self.stream.wait_stream(torch.cuda.current_stream())
+        for st in self.streams:
+            st.wait_stream(torch.cuda.current_stream())
 
 
 class HostSink:

@@ -67,11 +67,13 @@ def main():
             print(json.dumps({"ablation": "sched", "workload": "MIX (4 groups x 16, 1024-token prefixes, pool 2600)",
                               "policy": policy, **r}))
     if a.which in ("fsm", "all"):
-        for comp in (True, False):
-            r = _time(workloads.json_decode(compressed=comp), dev, flush, a.steps, a.warmup)
-            # output tokens include the start edge prefilled with the prompt (compressed mode)
-            print(json.dumps({"ablation": "fsm", "workload": "JSON (64 req, 512-token shared instruction, "
-                              "character-profile regex)", "compressed": comp, **r}))
+        for n_req, prefix in ((64, 512), (256, 1024)):
+            for comp in (True, False):
+                r = _time(workloads.json_decode(n_req=n_req, prefix=prefix, compressed=comp), dev, flush, a.steps,
+                          a.warmup)
+                # output tokens include the start edge prefilled with the prompt (compressed mode)
+                print(json.dumps({"ablation": "fsm", "workload": f"JSON ({n_req} req, {prefix}-token shared "
+                                  "instruction, character-profile regex)", "compressed": comp, **r}))
 
 
 if __name__ == "__main__":

@@ -47,7 +47,7 @@ def main():
     ei = 0
     dec_ms, dec_n, dec_bytes = 0.0, 0, 0.0
     kern_ms = 0.0
-    for kind, ev0, ev1, work, nl in eng.timer:
+    for kind, ev0, ev1, work, nl, calls in eng.timer:
         ms = ev0.elapsed_time(ev1)
         kern_ms += ms
         if kind == "extend":
@@ -59,8 +59,8 @@ def main():
                   f"max={pre.max():6d}: {ms:8.3f} ms {work / ms / 1e9:7.1f} TFLOP/s launches={nl}")
         else:
             dec_ms += ms
-            dec_n += 1
-            dec_bytes += eng.decode_bytes(work)[0]
+            dec_n += calls
+            dec_bytes += sum(eng.decode_bytes(w)[0] for w in work)
     if dec_n:
         print(f"decode: {dec_n} calls {dec_ms:.2f} ms {dec_bytes / dec_ms / 1e6:.1f} GB/s (algorithmic)")
     print(f"pass {total:.2f} ms, kernels (event-bracketed) {kern_ms:.2f} ms, gaps {total - kern_ms:.2f} ms")

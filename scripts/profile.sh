@@ -1,18 +1,20 @@
 #!/usr/bin/env bash
 # Profiling recipe (run under gpurun on ONE GPU; see /opt/skills/guides/B200_PROFILING.md).
-#   bash scripts/profile.sh [workload] [kernel-regex]
+#   bash scripts/profile.sh [workload] [kernel-regex] [skip] [count]
 # Writes to gpurun_out/:
 #   launches_<wl>.csv   every launch of one bench step with its device time (cold-cache, serialised)
 #   full_<wl>_<k>.ncu-rep   one `--set full` capture of the chosen kernel
 set -u
 WL=${1:-C3}
 K=${2:-decode_kernel}
+SKIP=${3:-20}
+CNT=${4:-2}
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout -k 5 1500 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${WL}.csv \
-  python bench.py --workload "$WL" --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/launches_${WL}.stdout 2>&1
-timeout -k 5 900 $NCU --set full --clock-control none --import-source on -k "regex:${K}" -s 20 -c 2 \
+  python bench.py --workload "$WL" --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --secondary none > gpurun_out/launches_${WL}.stdout 2>&1
+timeout -k 5 900 $NCU --set full --clock-control none --import-source on -k "regex:${K}" -s ${SKIP} -c ${CNT} \
   -o gpurun_out/full_${WL}_${K} -f \
-  python bench.py --workload "$WL" --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/full_${WL}_${K}.stdout 2>&1
+  python bench.py --workload "$WL" --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --secondary none > gpurun_out/full_${WL}_${K}.stdout 2>&1
 echo "profile done"

@@ -172,7 +172,7 @@ def test_host_io_path_bitwise_equal():
     e.run_workload(bank)
     torch.cuda.synchronize()
     ref = [o.cpu() for _, o, _ in e.outputs]
-    hb = HostInputs(bank, torch.device("cuda"), ext_depth=1, dec_depth=3)
+    hb = HostInputs(bank, torch.device("cuda"), ext_depth=1, dec_block=3, dec_depth=2)
     sink = HostSink([torch.empty((len(c.hashes), wl.shape.h_q, wl.shape.head_dim), dtype=torch.bfloat16,
                                  pin_memory=True) for c in plan.calls], torch.device("cuda"))
     e2 = Engine(wl, "cuda")
