@@ -262,7 +262,10 @@ def main():
                        "dram_bytes_per_captured_launch": tj["dram_bytes_per_launch"],
                        "algorithmic_bytes_per_captured_launch": tj["algorithmic_bytes_per_launch"],
                        "ratio": tj["traffic_over_algorithmic"]}
+    # SURVEY §8(d) "always report both" denominators: the measured peak (frac) and the nominal one
+    nominal = 2250.0 if kind == "extend" else 8000.0            # TFLOP/s dense bf16 | GB/s HBM3e
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
+                 "nominal_peak": nominal, "frac_nominal": achieved / nominal,
                  "traffic_source": traffic_src,
                  "peak_source": f"{peak_src} MEASURED_PEAKS.json" if peak_src == "measured" else "fallback",
                  "share_of_step": kms / total_ms if world == 1 else None})

@@ -113,6 +113,7 @@ class Engine:
         self.shape = wl.shape
         self.device = device
         self.plan_only = plan_only
+        self.collect_calls = True             # plan pass: record per-call row hashes (input generation)
         self.record = record
         self.keep_outputs = keep_outputs
         self.gather = gather                  # callable(local o) -> full o, or None (P == 1)
@@ -376,7 +377,7 @@ class Engine:
                 steps.append(("dec", running, new, pos))
                 if self.on_decode_plan is not None:
                     self.on_decode_plan(self, slots, running, pos)
-                if self.plan_only:
+                if self.plan_only and self.collect_calls:
                     hs = np.array([rs[b].hashes[p_] for b, p_ in zip(running, pos)], dtype=np.uint64)
                     self.calls.append(CallPlan("decode", hs, {"B": len(running)}))
             else:
@@ -385,7 +386,7 @@ class Engine:
                     slots[b, p_:p_ + n_] = new[o_:o_ + n_]
                     o_ += n_
                 steps.append(("ext", running, pos, lens))
-                if self.plan_only:
+                if self.plan_only and self.collect_calls:
                     hs = np.concatenate([rs[b].hashes[p_:p_ + n_] for b, p_, n_ in zip(running, pos, lens)])
                     self.calls.append(CallPlan("extend", hs.astype(np.uint64), {"ext": lens.tolist()}))
             cur[running] += lens
@@ -441,6 +442,8 @@ class Engine:
         B = len(rs)
         self.stats["extend_tokens"] += total
         if self.plan_only:
+            if not self.collect_calls:
+                return
             hs = np.array([h for r, n in zip(rs, ext) for h in r.hashes[r.prefix:r.prefix + n]], dtype=np.uint64)
             self.calls.append(CallPlan("extend", hs, {"ext": ext.tolist(), "prefix": prefix.tolist()}))
             return

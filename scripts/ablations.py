@@ -69,8 +69,8 @@ def main():
     if a.which in ("fsm", "all"):
         for n_req, prefix in ((64, 512), (256, 1024)):
             for comp in (True, False):
-                r = _time(workloads.json_decode(n_req=n_req, prefix=prefix, compressed=comp), dev, flush, a.steps,
-                          a.warmup)
+                r = _time(workloads.json_decode(n_req=n_req, prefix=prefix, compressed=comp, num_slots=1 << 18), dev,
+                          flush, a.steps, a.warmup)
                 # output tokens include the start edge prefilled with the prompt (compressed mode)
                 print(json.dumps({"ablation": "fsm", "workload": f"JSON ({n_req} req, {prefix}-token shared "
                                   "instruction, character-profile regex)", "compressed": comp, **r}))

@@ -21,7 +21,15 @@ def main():
     sink = HostSink([torch.empty((len(c.hashes), wl.shape.h_q, wl.shape.head_dim), dtype=torch.bfloat16,
                                  pin_memory=True) for c in plan.calls], dev)
     flush = torch.empty(2 * torch.cuda.get_device_properties(dev).L2_cache_size, dtype=torch.uint8, device=dev)
-    for name, inputs, sk in (("device", bank, None), ("h2d", hb, None), ("d2h", bank, sink), ("both", hb, sink)):
+    # "copy||": every H2D block copy issued up front on the copy streams while the kernels run from
+    # the device-resident bank (no dependency): do copies and kernels overlap at all?
+    def all_copies():
+        for i in range(len(hb.ext.lst)):
+            hb.ext._issue(i)
+        for j in range(len(hb.dec.ranges)):
+            hb.dec._issue(j)
+    for name, inputs, sk in (("device", bank, None), ("copy||", bank, None), ("h2d", hb, None),
+                             ("d2h", bank, sink), ("both", hb, sink)):
         eng.sink = sk
         ts = []
         for i in range(4):
@@ -30,12 +38,17 @@ def main():
             a, b = torch.cuda.Event(True), torch.cuda.Event(True)
             sink.reset()
             a.record()
-            if inputs is hb:
+            if inputs is hb or name == "copy||":
                 hb.reset()
+            if name == "copy||":
+                all_copies()
             eng.reset()
             eng.run_workload(inputs)
             if sk is not None:
                 sk.join()
+            if name == "copy||":
+                for st in hb.streams:
+                    torch.cuda.current_stream().wait_stream(st)
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))

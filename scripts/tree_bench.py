@@ -31,6 +31,7 @@ def main():
     ops = sum(1 for t in rec.trace if t[0] in ("match", "inc_ref", "alloc", "evict", "dec_ref", "insert"))
     best_lib, best_lib_tree = 1e9, 1e9
     e = Engine(wl, plan_only=True)
+    e.collect_calls = False                # tree ops only: no per-call input bookkeeping
     e.run_workload()                       # first pass also draws the mock-model token streams (cached)
     for _ in range(a.reps):
         e.reset()
