@@ -355,6 +355,27 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch,
                     void* d_k_pool, void* d_v_pool, int64_t num_slots, void* d_o,
                     void* d_ws, size_t ws_bytes, void* stream);
 
+/* rx_extend for a batch whose rows all share cached positions [0, shared_len)
+ * (the same slots, i.e. one radix-tree path: the running requests of a
+ * few-shot or long-context batch), for short segments (jump-forward steps,
+ * §4).  Same result as rx_extend (within the attention tolerance); the
+ * shared prefix is attended ONCE for all Σ extend_len rows on the tensor cores
+ * (cascade) and each request's own positions
+ * [shared_len, prefix_len + j] by the multi-query decode kernel, merged by
+ * log-sum-exp.  Preconditions: 0 <= shared_len <= every prefix_len and the
+ * slots of positions < shared_len equal in every row (not checked); when
+ * shared_len == 0 or the multi-query shape condition of rx_extend fails the
+ * call is exactly rx_extend.  Workspace: >= rx_extend_cascade_workspace_bytes
+ * (cfg, total_new, shared_len) bytes.  Four launches (store, suffix, shared,
+ * merge). */
+size_t rx_extend_cascade_workspace_bytes(const rx_attn_cfg* cfg, int64_t total_new, int32_t shared_len);
+rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
+                            const int32_t* d_rows, const int32_t* d_prefix_lens, const int32_t* d_extend_lens,
+                            const int32_t* d_qo_indptr, int64_t total_new, int32_t max_extend_len,
+                            int32_t max_prefix_len, int32_t shared_len, const void* d_q, const void* d_k_new,
+                            const void* d_v_new, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* d_o,
+                            void* d_ws, size_t ws_bytes, void* stream);
+
 size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len);
 
 /* Decode: one query per request at position seq_len[b] - 1 (P:495 [App.

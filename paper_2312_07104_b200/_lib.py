@@ -78,6 +78,9 @@ SIGNATURES = {
     "rx_extend": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, vp, i64, i32, i32,
                             vp, vp, vp, vp, vp, i64, vp, vp, sz, vp]),
     "rx_extend_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
+    "rx_extend_cascade": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, vp, i64, i32, i32, i32,
+                                    vp, vp, vp, vp, vp, i64, vp, vp, sz, vp]),
+    "rx_extend_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i64, i32]),
     "rx_decode": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, i64, vp, vp, sz, vp]),
     "rx_decode_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, i64,
                                    vp, vp, sz, vp]),

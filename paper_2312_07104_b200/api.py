@@ -363,6 +363,28 @@ def rx_extend(cfg: AttnCfg, rtt, rows, prefix_lens, extend_lens, qo_indptr, tota
     _check(st, "rx_extend")
 
 
+def rx_extend_cascade_workspace_bytes(cfg: AttnCfg, total_new: int, shared_len: int) -> int:
+    return lib.rx_extend_cascade_workspace_bytes(C.byref(cfg), total_new, shared_len)
+
+
+def rx_extend_cascade(cfg: AttnCfg, rtt, rows, prefix_lens, extend_lens, qo_indptr, total_new: int,
+                      max_extend_len: int, max_prefix_len: int, shared_len: int, q, k_new, v_new, k_pool, v_pool, o,
+                      ws=None, stream=None):
+    """rx_extend with the rows' common cached prefix [0, shared_len) attended once (include/rx.h)."""
+    import torch
+    batch = prefix_lens.shape[0]
+    ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    st = lib.rx_extend_cascade(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
+                               _dev(rows, torch.int32, "rows"), _dev(prefix_lens, torch.int32, "prefix_lens"),
+                               _dev(extend_lens, torch.int32, "extend_lens"), _dev(qo_indptr, torch.int32, "qo_indptr"),
+                               total_new, max_extend_len, max_prefix_len, shared_len, _dev(q, torch.bfloat16, "q"),
+                               _dev(k_new, torch.bfloat16, "k_new"), _dev(v_new, torch.bfloat16, "v_new"),
+                               _dev(k_pool, torch.bfloat16, "k_pool"), _dev(v_pool, torch.bfloat16, "v_pool"),
+                               k_pool.shape[0], _dev(o, torch.bfloat16, "o"), _dev(ws, None, "ws"), ws_bytes,
+                               _stream(stream))
+    _check(st, "rx_extend_cascade")
+
+
 def rx_decode(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int, q, k_pool, v_pool, o, ws=None, stream=None):
     import torch
     batch = seq_lens.shape[0]

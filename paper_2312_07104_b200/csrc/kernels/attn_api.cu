@@ -225,6 +225,107 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   return RX_OK;
 }
 
+// Multi-query cascade (rx_extend_cascade): rows = every new token of the batch.
+static rx::CascadePlan plan_extend_cascade(const rx_attn_cfg* cfg, int64_t total_new, int32_t shared_len) {
+  rx::CascadePlan pl = rx::plan_cascade(int(total_new), cfg->h_kv, cfg->h_q / cfg->h_kv, shared_len + 1, shared_len);
+  pl.total_splits = pl.n_sh + 1;
+  return pl;
+}
+
+size_t rx_extend_cascade_workspace_bytes(const rx_attn_cfg* cfg, int64_t total_new, int32_t shared_len) {
+  if (check_cfg(cfg) != RX_OK || total_new <= 0 || shared_len <= 0) return 0;
+  const rx::CascadePlan pl = plan_extend_cascade(cfg, total_new, shared_len);
+  const size_t n = size_t(total_new) * cfg->h_q * pl.total_splits;
+  return n * cfg->head_dim * sizeof(float) + n * sizeof(float) + 256;
+}
+
+rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
+                            const int32_t* d_rows, const int32_t* d_prefix_lens, const int32_t* d_extend_lens,
+                            const int32_t* d_qo_indptr, int64_t total_new, int32_t max_extend_len,
+                            int32_t max_prefix_len, int32_t shared_len, const void* d_q, const void* d_k_new,
+                            const void* d_v_new, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* d_o,
+                            void* d_ws, size_t ws_bytes, void* stream) {
+  rx_status s = check_cfg(cfg);
+  if (s != RX_OK) return s;
+  if (shared_len < 0 || total_new < 0 || batch < 0) return RX_E_INVALID;
+  const int G = cfg->h_q / cfg->h_kv;
+  if (shared_len == 0 || batch == 0 || total_new == 0 || !use_multi_query(G, batch, cfg->h_kv, max_extend_len))
+    return rx_extend(cfg, batch, d_rtt, rtt_stride, d_rows, d_prefix_lens, d_extend_lens, d_qo_indptr, total_new,
+                     max_extend_len, max_prefix_len, d_q, d_k_new, d_v_new, d_k_pool, d_v_pool, num_slots, d_o,
+                     d_ws, ws_bytes, stream);
+  if (!d_rtt || !d_prefix_lens || !d_extend_lens || !d_qo_indptr || !d_q || !d_k_new || !d_v_new || !d_k_pool ||
+      !d_v_pool || !d_o || num_slots < 1 || max_extend_len < 1)
+    return RX_E_INVALID;
+  if (rtt_stride < max_prefix_len || rtt_stride < max_extend_len || shared_len > max_prefix_len)
+    return RX_E_INVALID;
+  const size_t need = rx_extend_cascade_workspace_bytes(cfg, total_new, shared_len);
+  if (!d_ws || ws_bytes < need) return RX_E_WORKSPACE;
+  g_last_launches = 0;
+  const rx::CascadePlan pl = plan_extend_cascade(cfg, total_new, shared_len);
+  const size_t n = size_t(total_new) * cfg->h_q * pl.total_splits;
+  float* ws_o = static_cast<float*>(d_ws);
+  float* ws_lse = reinterpret_cast<float*>(static_cast<char*>(d_ws) + n * cfg->head_dim * sizeof(float));
+  const float scale_log2 = cfg->sm_scale * 1.4426950408889634f;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // A5: the new rows into their slots
+  cudaError_t e = rx::launch_extend_store(total_new, batch, cfg->h_kv * cfg->head_dim * 2, d_qo_indptr, d_extend_lens,
+                                          d_prefix_lens, d_rows, d_rtt, rtt_stride, d_k_new, d_v_new, d_k_pool,
+                                          d_v_pool, st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  // (1) each request's own positions [shared_len, prefix + j] on the multi-query decode kernel:
+  //     partial at split n_sh of every row
+  rx::DecodeParams dp{};
+  dp.q = static_cast<const __nv_bfloat16*>(d_q);
+  dp.kpool = static_cast<const __nv_bfloat16*>(d_k_pool);
+  dp.vpool = static_cast<const __nv_bfloat16*>(d_v_pool);
+  dp.o = static_cast<__nv_bfloat16*>(d_o);
+  dp.rtt = d_rtt;
+  dp.rtt_stride = rtt_stride;
+  dp.rows = d_rows;
+  dp.ws_o = ws_o;
+  dp.ws_lse = ws_lse;
+  dp.h_q = cfg->h_q;
+  dp.h_kv = cfg->h_kv;
+  dp.chunk = (max_prefix_len + max_extend_len + 15) / 16 * 16;
+  dp.max_splits = pl.total_splits;
+  dp.scale_log2 = scale_log2;
+  dp.qo_indptr = d_qo_indptr;
+  dp.prefix_lens = d_prefix_lens;
+  dp.col_tiles = (max_extend_len * G + 7) / 8;
+  dp.kv_start = shared_len;
+  dp.split_base = pl.n_sh;
+  dp.fixed_splits = pl.total_splits;
+  e = rx::launch_decode_multi(cfg->head_dim, G, dp, batch, st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  // (2) the shared prefix [0, shared_len) once for every row of the batch on tcgen05 (the rows are
+  //     one virtual request, no mask: every row's position is >= shared_len): splits [0, n_sh)
+  rx::ExtendParams ep{};
+  ep.rtt = d_rtt;
+  ep.rtt_stride = rtt_stride;
+  ep.rows = d_rows;
+  ep.kpool = static_cast<__nv_bfloat16*>(d_k_pool);
+  ep.vpool = static_cast<__nv_bfloat16*>(d_v_pool);
+  ep.h_q = cfg->h_q;
+  ep.h_kv = cfg->h_kv;
+  ep.num_slots = num_slots;
+  ep.scale_log2 = scale_log2;
+  ep.cascade = 1;
+  ep.kv_split_tiles = pl.kv_split_tiles;
+  ep.n_kv_splits = pl.n_sh;
+  ep.part_o = ws_o;
+  ep.part_lse = ws_lse;
+  ep.part_splits = pl.total_splits;
+  ep.part_base = 0;
+  ep.cas_prefix = shared_len;
+  e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, int(total_new), st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  // (3) log-sum-exp merge per row
+  e = rx::launch_decode_merge(cfg->head_dim, dp, int(total_new), st);
+  if (e != cudaSuccess) return RX_E_CUDA;
+  g_last_launches = 4;
+  return RX_OK;
+}
+
 size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len) {
   (void)cfg;
   (void)batch;

@@ -268,9 +268,15 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
       Ls += f * red_l[w][h];
       acc += f * opart[(w * HD + d) * 8 + h];
     }
-    if (MULTI) {   // one split: every column saw key 0, so Ls > 0
+    if (MULTI) {   // one split; every column saw >= 1 key (key 0, or its own position), so Ls > 0
       const int j = (ct * 8 + h) / G, hq = g * G + (ct * 8 + h) % G;
-      p.o[(int64_t(q0 + j) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / Ls);
+      if (p.split_base == 0) {
+        p.o[(int64_t(q0 + j) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / Ls);
+      } else {     // cascade: this is the suffix partial after split_base shared-prefix partials
+        const int64_t base = (int64_t(q0 + j) * p.h_q + hq) * p.max_splits + p.split_base;
+        p.ws_o[base * HD + d] = acc / Ls;
+        if (d == 0) p.ws_lse[base] = M + __log2f(Ls);
+      }
       continue;
     }
     const int hq = g * G + h;
@@ -288,8 +294,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
 template <int HD>
 __global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p) {
   const int b = blockIdx.x, hq = blockIdx.y;
-  const int L = p.seq_lens[b];
-  const int nsplit = p.split_base + (L - p.kv_start + p.chunk - 1) / p.chunk;
+  const int nsplit = p.fixed_splits > 0 ? p.fixed_splits
+                                        : p.split_base + (p.seq_lens[b] - p.kv_start + p.chunk - 1) / p.chunk;
   if (nsplit <= 1) return;
   const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits;
   float M = -INFINITY;

@@ -60,6 +60,10 @@ constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
 // Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
 // stores clock64 per (event code, item/tile index); read back with rx_debug_ext_trace().
 __device__ unsigned long long rx_ext_trace[16 * 1024];   // [code][item & 1023]: clock64, CTA 0 only
+// Dynamic work distribution: [0] = next work index, [1] = CTAs finished.  The last CTA of a launch
+// resets both, so the next launch on the stream starts from 0 (extend launches are stream-ordered;
+// two extend kernels must not run concurrently on one device).
+__device__ int rx_ext_sched[2];
 __device__ __forceinline__ void ext_trace(int on, int code, int item) {
   if (on && blockIdx.x == 0) rx_ext_trace[code * 1024 + (item & 1023)] = clock64();   // plain store, no wait
 }
@@ -523,26 +527,27 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     // ------------------------------------------------------------ item scheduler (+ TMEM owner)
     // (A5, storing the new K/V rows into their slots, is extend_store_kernel,
     // launched just before this kernel on the same stream.)
+    // Items are handed out dynamically: a CTA takes the next work index when a descriptor slot is
+    // free (it runs kRing items ahead), so ragged batches (requests of different lengths: items of
+    // 1..N tiles, some q tiles absent) balance across SMs; consecutive indices still start at
+    // about the same time on neighbouring CTAs, which keeps one (b, g)'s prefix L2-resident.
     RingCursor c;
-    const int stride = 32 * gridDim.x;
-    for (int base = blockIdx.x; base < W; base += stride) {
-      const int w = base + lane * gridDim.x;
+    for (;;) {
+      int w = 0;
+      if (lane == 0) w = atomicAdd(&rx_ext_sched[0], 1);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (w >= W) break;
       ExtItem I;
-      const bool v = w < W && ext_item<TOK>(p, qt, w, I);
-      unsigned m = __ballot_sync(0xffffffffu, v);
-      while (m) {
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        mbar_wait(desc_empty + c.slot, c.phase ^ 1);
-        if (lane == l) {
-          ring[c.slot] = I;
-          mbar_arrive(desc_full + c.slot);
-        }
-        __syncwarp();
-        if (++c.slot == kRing) {
-          c.slot = 0;
-          c.phase ^= 1;
-        }
+      if (!ext_item<TOK>(p, qt, w, I)) continue;
+      mbar_wait(desc_empty + c.slot, c.phase ^ 1);
+      if (lane == 0) {
+        ring[c.slot] = I;
+        mbar_arrive(desc_full + c.slot);
+      }
+      __syncwarp();
+      if (++c.slot == kRing) {
+        c.slot = 0;
+        c.phase ^= 1;
       }
     }
     mbar_wait(desc_empty + c.slot, c.phase ^ 1);      // sentinel
@@ -558,6 +563,14 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (threadIdx.x == 0) {   // every fetch of this CTA is done: the last CTA resets the scheduler
+    __threadfence();
+    if (atomicAdd(&rx_ext_sched[1], 1) == int(gridDim.x) - 1) {
+      rx_ext_sched[0] = 0;
+      rx_ext_sched[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side

@@ -44,6 +44,9 @@ struct DecodeParams {
   const int32_t* qo_indptr;
   const int32_t* prefix_lens;
   int col_tiles;
+  // merge: when > 0, every row has exactly this many partials (multi-query cascade:
+  // n_sh shared chunks + 1 suffix split) and seq_lens is not read
+  int fixed_splits;
 };
 
 struct ExtendParams {

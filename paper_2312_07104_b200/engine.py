@@ -37,6 +37,14 @@ from rxgen.values import gen_values, KIND_K, KIND_V, KIND_Q
 from . import api
 
 
+def _ragged_flat(starts, lens):
+    """concat(arange(s, s + n) for s, n in zip(starts, lens)) without a Python loop."""
+    lens = np.asarray(lens, dtype=np.int64)
+    total = int(lens.sum())
+    excl = np.cumsum(lens) - lens
+    return np.repeat(np.asarray(starts, dtype=np.int64) - excl, lens) + np.arange(total, dtype=np.int64)
+
+
 class OutOfSlots(RuntimeError):
     pass
 
@@ -140,6 +148,7 @@ class Engine:
         self.cascade_min_batch = 4
         self._shared = 0
         self._ws = None
+        self._rtt = None
         self._fsm = None                      # compressed FSM of the workload's regex (JSON workload)
         self.on_decode_plan = None            # callable(engine, slots, running, pos) per planned decode step
         self.launch_chunk = int(os.environ.get("RX_LAUNCH_CHUNK", "32"))   # output steps planned per launch batch
@@ -381,10 +390,7 @@ class Engine:
                     hs = np.array([rs[b].hashes[p_] for b, p_ in zip(running, pos)], dtype=np.uint64)
                     self.calls.append(CallPlan("decode", hs, {"B": len(running)}))
             else:
-                o_ = 0
-                for b, p_, n_ in zip(running, pos, lens):
-                    slots[b, p_:p_ + n_] = new[o_:o_ + n_]
-                    o_ += n_
+                slots.reshape(-1)[_ragged_flat(running.astype(np.int64) * slots.shape[1] + pos, lens)] = new
                 steps.append(("ext", running, pos, lens))
                 if self.plan_only and self.collect_calls:
                     hs = np.concatenate([rs[b].hashes[p_:p_ + n_] for b, p_, n_ in zip(running, pos, lens)])
@@ -453,9 +459,9 @@ class Engine:
         """A multi-token output step (jump forward): the running requests' segments
         (sampled token + forced edge) are processed by one extend call over their cached context
         (prefix = current length), table rows selected by `running`."""
-        self._extend_launch(slots, running, pos, lens)
+        self._extend_launch(slots, running, pos, lens, shared=self._shared)
 
-    def _extend_launch(self, slots, rows, prefix, ext):
+    def _extend_launch(self, slots, rows, prefix, ext, shared=0):
         """rx_extend over table `slots` (every row of the batch, uploaded whole so later decode
         steps index it by batch row); batch entry b uses row rows[b] (None = identity)."""
         dev = self.device
@@ -463,12 +469,15 @@ class Engine:
         total = int(ext.sum())
         q, k_new, v_new = self.bank.ext[self._ext_i]
         self._ext_i += 1
-        # one pinned staging block: [prefix | ext | qo_indptr | rows] then the rtt rows
         R, stride = slots.shape
-        hdr = 4 * (B + 1)
         name = f"ext{self._ext_ring % 8}"            # ring: the host may run several extends ahead
         self._ext_ring += 1
-        stage = self._pinned(name, hdr + R * stride)
+        # an output step (rows given) keeps the batch's device table and writes only its new slots
+        # into it (rx_store_kv's table append); a prefill uploads the table whole
+        incremental = rows is not None and self._rtt is not None and tuple(self._rtt.shape) == (R, stride)
+        tail = 3 * total if incremental else R * stride
+        hdr = 4 * (B + 1)
+        stage = self._pinned(name, hdr + tail)
         sn = stage.numpy()
         sn[0:B] = prefix
         sn[B + 1:2 * B + 1] = ext
@@ -476,10 +485,22 @@ class Engine:
         sn[2 * B + 3:3 * B + 3] = np.cumsum(ext)
         if rows is not None:
             sn[3 * B + 3:4 * B + 3] = rows
-        sn[hdr:] = slots.reshape(-1)
+        if incremental:
+            # [int64 flat table index (2 int32 words each) | int32 slot] of every new row
+            flat = _ragged_flat(np.asarray(rows, dtype=np.int64) * stride + prefix, ext)
+            new_slots = slots.reshape(-1)[flat]
+            o2 = hdr + (hdr & 1)                     # 8-byte alignment of the int64 block
+            sn[o2:o2 + 2 * total].view(np.int64)[:] = flat
+            sn[o2 + 2 * total:o2 + 3 * total] = new_slots
+        else:
+            sn[hdr:] = slots.reshape(-1)
         dstage = stage.to(dev, non_blocking=True)
         self._pinned_done(name)
-        self._rtt = dstage[hdr:].view(R, stride)
+        if incremental:
+            d_idx = dstage[o2:o2 + 2 * total].view(torch.int64)
+            d_new = dstage[o2 + 2 * total:o2 + 3 * total]
+        else:
+            self._rtt = dstage[hdr:].view(R, stride)
         self._B = R
         ws_n = api.rx_decode_workspace_bytes(self.cfg, R, stride)
         if self._ws is None or self._ws.numel() < ws_n:
@@ -487,7 +508,21 @@ class Engine:
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         chunks = self._gather_chunks(ext) if (self.gather is not None and hasattr(self.gather, "start")) else None
         ev0 = self._tbeg()
-        if chunks is None:
+        nl0 = 0
+        if incremental:
+            api.rx_store_kv(self.cfg, d_new, k_new, v_new, self.k_pool, self.v_pool, self._rtt, d_idx)
+            nl0 = api.rx_last_launch_count()
+        if chunks is None and shared > 0:
+            # every row shares cached positions [0, shared): attend them once for all rows (cascade)
+            ws_n = api.rx_extend_cascade_workspace_bytes(self.cfg, total, shared)
+            if self._ws.numel() < ws_n:
+                self._ws = torch.empty(2 * ws_n, dtype=torch.uint8, device=dev)
+            api.rx_extend_cascade(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
+                                  dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3], total,
+                                  int(ext.max()), int(prefix.max()), shared, q, k_new, v_new, self.k_pool,
+                                  self.v_pool, o, self._ws)
+            nl = api.rx_last_launch_count()
+        elif chunks is None:
             api.rx_extend(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
                           dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
                           total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o)
@@ -525,7 +560,7 @@ class Engine:
                               v_new[r0:r1], self.k_pool, self.v_pool, o[r0:r1])
                 nl += api.rx_last_launch_count()
                 handles.append(self.gather.start(o[r0:r1], out, r0, r1))
-        self.stats["launches"] += nl
+        self.stats["launches"] += nl + nl0
         if ev0 is not None:
             # algorithmic FLOPs: 4*hd*H_q*sum(n*p + n(n+1)/2), causal-masked work not counted
             n, p_ = ext.astype(np.float64), prefix.astype(np.float64)

@@ -25,6 +25,9 @@ def main():
     ap.add_argument("--ext", type=int, default=512)
     ap.add_argument("--shared-prefix", action="store_true")
     ap.add_argument("--scatter", action="store_true", help="fragmented (non-contiguous) slots")
+    ap.add_argument("--ragged", action="store_true", help="extend: prefix U[P/2, 3P/2], ext U[2E/3, 4E/3] per request")
+    ap.add_argument("--half", action="store_true", help="extend: scatter every other 384-token run of the prefix "
+                    "(C3 history: contiguous inputs, interleaved decode outputs)")
     ap.add_argument("--cascade", type=int, default=0, help="decode: shared prefix length (cascade vs per-request)")
     ap.add_argument("--iters", type=int, default=20)
     a = ap.parse_args()
@@ -97,6 +100,43 @@ def main():
         logical = B * L * h_kv * hd * 4
         print(f"decode {h_q}/{h_kv}/{hd} B={B} L={L}: {ms*1e3:.1f} us  alg {byt/ms/1e6:.0f} GB/s  "
               f"logical {logical/ms/1e6:.0f} GB/s  tokens/s {B/ms*1e3:.3e}")
+    elif a.kind == "extend" and (a.ragged or a.half):
+        import numpy as np
+        r = np.random.default_rng(0)
+        Ps = r.integers(a.prefix // 2, a.prefix * 3 // 2 + 1, B) if a.ragged else np.full(B, a.prefix)
+        Es = r.integers(a.ext * 2 // 3, a.ext * 4 // 3 + 1, B) if a.ragged else np.full(B, a.ext)
+        tot = int((Ps + Es).sum())
+        S = tot + 16
+        kp = torch.randn((S, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
+        vp = torch.randn_like(kp)
+        stride = int((Ps + Es).max())
+        rtt_h = np.zeros((B, stride), dtype=np.int32)
+        base = 1
+        for b in range(B):
+            n = int(Ps[b] + Es[b])
+            rtt_h[b, :n] = np.arange(base, base + n)
+            base += n
+        if a.half:       # every other 384-token run of every prefix: slots permuted across requests
+            mask = np.zeros((B, stride), dtype=bool)
+            for b in range(B):
+                for s0 in range(384, int(Ps[b]), 768):
+                    mask[b, s0:min(s0 + 384, int(Ps[b]))] = True
+            vals = rtt_h[mask]
+            rtt_h[mask] = vals[r.permutation(len(vals))]
+        rtt = torch.from_numpy(rtt_h).to(dev)
+        N = int(Es.sum())
+        q = torch.randn((N, h_q, hd), device=dev, generator=g).to(torch.bfloat16)
+        kn = torch.randn((N, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
+        vn = torch.randn_like(kn)
+        o = torch.empty_like(q)
+        pre = torch.from_numpy(Ps.astype(np.int32)).to(dev)
+        ext = torch.from_numpy(Es.astype(np.int32)).to(dev)
+        ind = torch.from_numpy(np.concatenate([[0], np.cumsum(Es)]).astype(np.int32)).to(dev)
+        ms = timeit(lambda: rx.rx_extend(cfg, rtt, None, pre, ext, ind, N, int(Es.max()), int(Ps.max()), q, kn, vn,
+                                         kp, vp, o))
+        flops = 4 * hd * h_q * float(np.sum(Es * Ps + Es * (Es + 1) / 2))
+        print(f"extend {h_q}/{h_kv}/{hd} B={B} P~{a.prefix} E~{a.ext} ragged={a.ragged} half={a.half}: "
+              f"{ms*1e3:.1f} us  {flops/ms/1e9:.1f} TFLOP/s tokens/s {N/ms*1e3:.3e}")
     elif a.kind == "extend":
         P, E = a.prefix, a.ext
         S = P + B * E + 16 if a.shared_prefix else B * (P + E) + 16

@@ -122,6 +122,32 @@ def test_c5_full_size_sampled():
     _compare(e, wl, re, rd)
 
 
+def test_c3_full_size_sampled():
+    """BASELINE C3 at full size — the workload and launch configuration bench.py times (256 sessions
+    x 4 turns, 786 k attention rows, 2045 decode steps): tree trace bit-exact over the whole run,
+    sampled attention rows of every extend (4 requests x 3 rows) and of the first, a middle and the
+    last decode step of every turn (3 requests each) within tolerance."""
+    wl = workloads.c3()
+
+    def re(call, seqs):
+        out = []
+        for i in (0, len(seqs) // 3, len(seqs) - 1, 97 % len(seqs)):
+            n = seqs[i].n_prompt - seqs[i].prefix_len
+            out += [(i, j) for j in sorted({0, n // 2, n - 1})]
+        return out
+
+    def rd(call, step, running):
+        # steps 0, 255 and the last steps of a turn (batch shrinks as sessions finish)
+        if step in (0, 255) or len(running) <= 2:
+            return sorted({0, len(running) // 2, len(running) - 1})
+        return []
+
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, re, rd)
+    assert oe.trace == e.trace
+    assert sum(1 for k in oe.outputs if k[0] == "decode") >= 12
+
+
 def test_c4_tot_full_parity():
     """C4 at full size: tree-of-thought under Alg. 1 admission with the pool at
     60% of the tree's distinct tokens (evictions between waves)."""

@@ -398,3 +398,57 @@ def _decode_append_check(h_q, h_kv, hd, lens):
     torch.cuda.synchronize()
     assert torch.equal(kp1, kp2) and torch.equal(vp1, vp2) and torch.equal(rtt1, rtt2)
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,B,shared,max_pre_own,max_ext", [
+    (32, 32, 128, 12, 700, 200, 20),     # G=1, up to 3 column tiles, shared 700 (not a tile multiple)
+    (32, 8, 128, 40, 1024, 90, 8),       # G=4
+    (64, 8, 128, 24, 300, 50, 4),        # G=8
+    (8, 2, 64, 80, 129, 40, 8),          # hd 64
+])
+@pytest.mark.parametrize("q_scale", [1.0, 4.0])
+def test_extend_cascade_vs_oracle(h_q, h_kv, hd, B, shared, max_pre_own, max_ext, q_scale):
+    """rx_extend_cascade: rows of B requests that share cached positions [0, shared) (same slots)
+    plus their own cached tokens and a short new segment: shared part once on tcgen05, own part on
+    the multi-query decode kernel, LSE merge — against the fp64 oracle, every row."""
+    rng = np.random.default_rng(B + shared + hd)
+    own = [int(x) for x in rng.integers(0, max_pre_own + 1, B)]
+    ext = [int(x) for x in rng.integers(1, max_ext + 1, B)]
+    ext[0] = max_ext
+    pre = [shared + o_ for o_ in own]
+    S = shared + sum(own) + sum(ext) + 64
+    stride = max(p + e for p, e in zip(pre, ext)) + 5
+    free = list(rng.permutation(np.arange(1, S)))
+    rtt = np.zeros((B, stride), dtype=np.int32)
+    sh_slots = free[:shared]
+    off = shared
+    for b in range(B):
+        rtt[b, :shared] = sh_slots
+        n = own[b] + ext[b]
+        rtt[b, shared:shared + n] = free[off:off + n]
+        off += n
+    kpool = _vals(rng, S, h_kv, KIND_K, hd)
+    vpool = _vals(rng, S, h_kv, KIND_V, hd)
+    N = sum(ext)
+    q = _vals(rng, N, h_q, KIND_Q, hd, scale=q_scale)
+    kn = _vals(rng, N, h_kv, KIND_K, hd)
+    vn = _vals(rng, N, h_kv, KIND_V, hd)
+    indptr = np.concatenate([[0], np.cumsum(ext)]).astype(np.int32)
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    kp, vp = kpool.cuda(), vpool.cuda()
+    o = torch.full((N, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(rx.rx_extend_cascade_workspace_bytes(cfg, N, shared), dtype=torch.uint8, device="cuda")
+    rows = torch.arange(B, dtype=torch.int32, device="cuda")
+    rx.rx_extend_cascade(cfg, torch.from_numpy(rtt).cuda(), rows, torch.tensor(pre, dtype=torch.int32, device="cuda"),
+                         torch.tensor(ext, dtype=torch.int32, device="cuda"), torch.from_numpy(indptr).cuda(), N,
+                         max(ext), max(pre), shared, q.cuda(), kn.cuda(), vn.cuda(), kp, vp, o, ws)
+    torch.cuda.synchronize()
+    assert rx.rx_last_launch_count() == 4                      # the cascade path ran
+    pool = A.OraclePool(S, h_kv, hd)
+    pool.store(np.arange(S), kpool.float().numpy(), vpool.float().numpy())
+    ref = A.extend(pool, [rtt[b] for b in range(B)], pre, ext, q.float().numpy(), kn.float().numpy(),
+                   vn.float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
+    _cmp(o, ref, f"extend_cascade {h_q}/{h_kv}/{hd} B={B} shared={shared}")
+    for b in range(B):
+        s_new = torch.from_numpy(rtt[b, pre[b]:pre[b] + ext[b]].astype(np.int64)).cuda()
+        assert torch.equal(kp[s_new], kn[indptr[b]:indptr[b + 1]].cuda())
