@@ -172,7 +172,11 @@ def main():
 
     import torch
     import torch.distributed as dist
-    if world > 1:
+    # RX_BENCH_TP_SELFTEST=1 under `torchrun --nproc-per-node 1`: run the TP code path (NCCL group,
+    # per-call output all-gather, chunked extend gathers, max-over-ranks) on one GPU — a check of
+    # the multi-GPU plumbing, not a scaling number
+    tp_path = world > 1 or (os.environ.get("RX_BENCH_TP_SELFTEST") == "1" and "RANK" in os.environ)
+    if tp_path:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -183,7 +187,7 @@ def main():
     from paper_2312_07104_b200.tp import make_gather
 
     wl = make_workload(args.workload)
-    gather = make_gather() if world > 1 else None
+    gather = make_gather() if tp_path else None
     plan, bank = plan_and_bank(wl, dev, tp_rank=rank, tp_size=world)
     eng = Engine(wl, dev, tp_rank=rank, tp_size=world, gather=gather)
     tokens = plan.stats["extend_tokens"] + plan.stats["decode_tokens"]
@@ -192,7 +196,7 @@ def main():
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
 
     def barrier():
-        if world > 1:
+        if tp_path:
             dist.barrier()
 
     def step():
@@ -228,7 +232,7 @@ def main():
                     t[i] += v_[i]
     launches = eng.stats["launches"]
     total_ms = sum(times)
-    if world > 1:
+    if tp_path:
         tt = torch.tensor([total_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
@@ -307,7 +311,7 @@ def main():
             e2e_times.append(a.elapsed_time(b))
         eng.sink = None
         e_ms = sum(e2e_times)
-        if world > 1:
+        if tp_path:
             tt = torch.tensor([e_ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())
@@ -349,7 +353,7 @@ def main():
                 for i in range(4):
                     t[i] += v_[i]
         ms2 = sum(t2)
-        if world > 1:
+        if tp_path:
             tt = torch.tensor([ms2], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms2 = float(tt.item())
@@ -377,14 +381,14 @@ def main():
                        "tokens_per_step": tokens, "extend_tokens": plan.stats["extend_tokens"],
                        "decode_tokens": plan.stats["decode_tokens"],
                        "cache_hit_rate": plan.stats["cached_prompt_tokens"] / max(1, plan.stats["prompt_tokens"]),
-                       "parallelism": f"tp{world}" if world > 1 else "single", "l2_flush": "2x L2 write before each timed step",
+                       "parallelism": f"tp{world}" if world > 1 else ("tp1-selftest" if tp_path else "single"), "l2_flush": "2x L2 write before each timed step",
                        "num_slots": wl.num_slots},
             "gpu_launches": launches, "roofline": roof, "kernels": kernels,
             "tree_ms_per_step": tree_s * 1000.0 / args.steps,
             "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "secondary": secondary,
         }
         print(json.dumps(line))
-    if world > 1:
+    if tp_path:
         dist.destroy_process_group()
 
 

@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   // into the pool slot (A5) and, for kv head 0, appends the slot to the
   // req_to_token row (A4); position L-1 then reads its slot from the argument,
   // never from the table, so no CTA races the table write.
+  // PDL (launch_decode): nothing below may read the pool, the table or the workspace before the
+  // preceding grid (the previous step's decode / merge) has completed
+  pdl_wait();
   const bool append = !MULTI && p.new_slots != nullptr;
   const int new_slot = append ? p.new_slots[b] : 0;
   if (append && s == nsplit - 1) {
@@ -230,6 +233,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
     __syncwarp();
   }
   cp_async_wait<0>();
+  pdl_launch_dependents();   // this CTA's streaming is done: let the next grid's CTAs fill the SM
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -293,6 +297,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
 // Log-sum-exp merge of split partials (A8): o = sum_s 2^(lse_s - LSE) o_s.
 template <int HD>
 __global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p) {
+  pdl_wait();                // the partials of the preceding grid(s) are complete
+  pdl_launch_dependents();   // ... so the next step may start (it waits for this merge in turn)
   const int b = blockIdx.x, hq = blockIdx.y;
   const int nsplit = p.fixed_splits > 0 ? p.fixed_splits
                                         : p.split_base + (p.seq_lens[b] - p.kv_start + p.chunk - 1) / p.chunk;
@@ -309,6 +315,33 @@ __global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p)
   }
 }
 
+// Programmatic dependent launch: decode steps and merges follow each other back to back; with
+// programmaticStreamSerialization the next grid is scheduled while the previous one drains (its
+// CTAs run their prologue, then griddepcontrol.wait).  RX_PDL=0 launches them plainly (A/B knob).
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RX_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+template <typename Kern>
+static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const DecodeParams& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 template <int HD, int G, int STAGES>
 static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_t st, int* launches) {
   using C = DecCfg<HD, STAGES>;
@@ -318,10 +351,12 @@ static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_
     attr = true;
   }
   dim3 grid(p.max_splits - p.split_base, p.h_kv, batch);   // suffix splits (cascade: shared partials come first)
-  decode_kernel<HD, G, STAGES><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);
+  cudaError_t e = launch_pdl(decode_kernel<HD, G, STAGES>, grid, dim3(kDecWarps * 32), C::SMEM, st, p);
+  if (e != cudaSuccess) return e;
   *launches = 1;
   if (p.max_splits > 1 && p.split_base == 0) {   // cascade: the caller merges after the shared part
-    decode_merge_kernel<HD><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
+    e = launch_pdl(decode_merge_kernel<HD>, dim3(batch, p.h_q), dim3(128), 0, st, p);
+    if (e != cudaSuccess) return e;
     *launches = 2;
   }
   return cudaPeekAtLastError();
