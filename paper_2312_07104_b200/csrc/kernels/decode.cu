@@ -295,24 +295,52 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
 }
 
 // Log-sum-exp merge of split partials (A8): o = sum_s 2^(lse_s - LSE) o_s.
+// One warp per (row, q head), 8 per CTA: each lane owns HD/32 consecutive dims (float2/float4
+// reads of every split's partial), the split weights are computed once per warp.
+constexpr int kMergeWarps = 8;
+
 template <int HD>
-__global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const DecodeParams p, int rows) {
   pdl_wait();                // the partials of the preceding grid(s) are complete
   pdl_launch_dependents();   // ... so the next step may start (it waits for this merge in turn)
-  const int b = blockIdx.x, hq = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int64_t pair = int64_t(blockIdx.x) * kMergeWarps + (threadIdx.x >> 5);
+  if (pair >= int64_t(rows) * p.h_q) return;
+  const int b = int(pair / p.h_q);
   const int nsplit = p.fixed_splits > 0 ? p.fixed_splits
                                         : p.split_base + (p.seq_lens[b] - p.kv_start + p.chunk - 1) / p.chunk;
   if (nsplit <= 1) return;
-  const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits;
+  const int64_t base = pair * p.max_splits;
   float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, p.ws_lse[base + s]);
+  for (int s = lane; s < nsplit; s += 32) M = fmaxf(M, p.ws_lse[base + s]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  constexpr int V = HD / 32;                       // 4 (hd 128) or 2 (hd 64) floats per lane
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
   float W = 0.f;
-  for (int s = 0; s < nsplit; ++s) W += fast_exp2(p.ws_lse[base + s] - M);
-  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < nsplit; ++s) acc += fast_exp2(p.ws_lse[base + s] - M) * p.ws_o[(base + s) * HD + d];
-    p.o[(int64_t(b) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / W);
+  for (int s = 0; s < nsplit; ++s) {
+    const float w = fast_exp2(p.ws_lse[base + s] - M);
+    W += w;
+    const float* src = p.ws_o + (base + s) * HD + lane * V;
+    if constexpr (V == 4) {
+      const float4 x = *reinterpret_cast<const float4*>(src);
+      acc[0] += w * x.x, acc[1] += w * x.y, acc[2] += w * x.z, acc[3] += w * x.w;
+    } else {
+      const float2 x = *reinterpret_cast<const float2*>(src);
+      acc[0] += w * x.x, acc[1] += w * x.y;
+    }
   }
+  const float inv = 1.f / W;
+  __nv_bfloat16* dst = p.o + pair * HD + lane * V;
+#pragma unroll
+  for (int v = 0; v < V; v += 2)
+    *reinterpret_cast<uint32_t*>(dst + v) = pack_bf16(acc[v] * inv, acc[v + 1] * inv);
+}
+
+static dim3 merge_grid(int rows, int h_q) {
+  return dim3(unsigned((int64_t(rows) * h_q + kMergeWarps - 1) / kMergeWarps));
 }
 
 // Programmatic dependent launch: decode steps and merges follow each other back to back; with
@@ -327,8 +355,8 @@ static bool pdl_enabled() {
   return v != 0;
 }
 
-template <typename Kern>
-static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const DecodeParams& p) {
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -339,7 +367,7 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cud
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 template <int HD, int G, int STAGES>
@@ -355,7 +383,7 @@ static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_
   if (e != cudaSuccess) return e;
   *launches = 1;
   if (p.max_splits > 1 && p.split_base == 0) {   // cascade: the caller merges after the shared part
-    e = launch_pdl(decode_merge_kernel<HD>, dim3(batch, p.h_q), dim3(128), 0, st, p);
+    e = launch_pdl(decode_merge_kernel<HD>, merge_grid(batch, p.h_q), dim3(kMergeWarps * 32), 0, st, p, batch);
     if (e != cudaSuccess) return e;
     *launches = 2;
   }
@@ -386,8 +414,8 @@ cudaError_t launch_decode_multi(int head_dim, int G, const DecodeParams& p, int 
 }
 
 cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st) {
-  if (head_dim == 64) decode_merge_kernel<64><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
-  else decode_merge_kernel<128><<<dim3(batch, p.h_q), 128, 0, st>>>(p);
+  if (head_dim == 64) decode_merge_kernel<64><<<merge_grid(batch, p.h_q), kMergeWarps * 32, 0, st>>>(p, batch);
+  else decode_merge_kernel<128><<<merge_grid(batch, p.h_q), kMergeWarps * 32, 0, st>>>(p, batch);
   return cudaPeekAtLastError();
 }
 

@@ -7,6 +7,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 
 namespace rx {
 
@@ -121,13 +122,25 @@ struct CascadePlan {
   int total_splits;
 };
 
+// Items per SM the shared-prefix split aims at (extend items are handed out dynamically, so more,
+// smaller items trade per-item overhead for a shorter tail).  RX_CASCADE_IPS overrides (A/B knob).
+inline int cascade_items_per_sm() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RX_CASCADE_IPS");
+    v = e ? atoi(e) : 2;
+    if (v < 1 || v > 32) v = 2;
+  }
+  return v;
+}
+
 inline CascadePlan plan_cascade(int batch, int h_kv, int group, int max_seq_len, int shared_len) {
   CascadePlan c{};
   const int tok = 128 / group;
   const int qt = (batch + tok - 1) / tok;
   const int tiles = (shared_len + 127) / 128;
   const int per_chunk = qt * h_kv;
-  int n = (2 * 148 + per_chunk - 1) / per_chunk;
+  int n = (cascade_items_per_sm() * 148 + per_chunk - 1) / per_chunk;
   n = n < 1 ? 1 : (n > tiles ? tiles : n);
   c.kv_split_tiles = (tiles + n - 1) / n;
   c.n_sh = (tiles + c.kv_split_tiles - 1) / c.kv_split_tiles;
