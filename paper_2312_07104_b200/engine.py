@@ -139,7 +139,8 @@ class Engine:
         self.bank = None
         self._full_cache = {}
         self.timer = None
-        self._pin_cache = {}
+        self._pin_cache = {}                 # name -> pinned buffer checked out
+        self._pin_pool = []                   # (pinned buffer, event of its last H2D copy)
         self.sink = None                     # callable(kind, o) invoked after every attention call
         self.evict_listener = None           # callable(path tokens, leaf_start) per evicted leaf (DP workers)
         # shared-prefix (cascade) decode when the batch shares >= cascade_min_len cached slots
@@ -649,20 +650,29 @@ class Engine:
 
     # ------------------------------------------------------------------ pinned staging
     def _pinned(self, name, n):
-        """Grow-only pinned int32 staging buffer; waits for its previous H2D copy before reuse."""
-        buf, ev = self._pin_cache.get(name, (None, None))
-        if ev is not None:
-            ev.synchronize()
-        if buf is None or buf.numel() < n:
-            buf = torch.empty(max(n, 1024), dtype=torch.int32, pin_memory=True)
-        self._pin_cache[name] = (buf, None)
+        """Pinned int32 staging buffer of >= n elements from a pool: any buffer whose last H2D copy
+        has completed is reused (smallest that fits), so steady state allocates nothing — pinned
+        allocation (cudaHostAlloc) takes milliseconds.  `name` tags the checkout for _pinned_done."""
+        pool = self._pin_pool
+        best = None
+        for i, (buf, ev) in enumerate(pool):
+            if buf.numel() >= n and (ev is None or ev.query()):
+                if best is None or buf.numel() < pool[best][0].numel():
+                    best = i
+        if best is None:
+            buf = torch.empty(max(n, 1 << 16), dtype=torch.int32, pin_memory=True)
+        else:
+            buf, _ = pool.pop(best)
+        self._pin_cache[name] = buf
         return buf[:n]
 
     def _pinned_done(self, name):
-        buf, _ = self._pin_cache[name]
+        """The H2D copy from the buffer checked out as `name` is enqueued: return it to the pool,
+        reusable once that copy has run."""
+        buf = self._pin_cache.pop(name)
         ev = torch.cuda.Event()
         ev.record()
-        self._pin_cache[name] = (buf, ev)
+        self._pin_pool.append((buf, ev))
 
     # ------------------------------------------------------------------ timing hooks
     def enable_timing(self, on=True):
