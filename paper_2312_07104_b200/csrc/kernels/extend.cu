@@ -413,17 +413,21 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         // Scores stay raw (unscaled); the scale is folded into the exp2 FFMA.
         const int lim = j < I.n_pre ? I.P - (I.tile0 + j) * kBN - 1 : rel - (j - I.n_pre) * kBN;
         const bool full = __all_sync(0xffffffffu, lim >= kBN - 1);   // warp-uniform
-        float mx = -INFINITY;
-        if (full) {
+        // row max over 128 columns as 8 independent chains (one softmax warp per SM sub-partition:
+        // a single 64-deep FMNMX3 dependency chain would leave the SMSP idle on ALU latency)
+        if (!full) {
 #pragma unroll
-          for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, sv[c]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < kBN; ++c) {
-            sv[c] = c <= lim ? sv[c] : -INFINITY;
-            mx = fmaxf(mx, sv[c]);
-          }
+          for (int c = 0; c < kBN; ++c) sv[c] = c <= lim ? sv[c] : -INFINITY;
         }
+        float mxp[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mxp[k] = fmaxf(sv[k], sv[k + 8]);
+#pragma unroll
+        for (int c = 16; c < kBN; c += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mxp[k] = fmaxf(mxp[k], fmaxf(sv[c + k], sv[c + k + 8]));
+        float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                         fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
         mx *= p.scale_log2;
         // Lazy rescale, decided per WARP: tcgen05.ld/st are .sync.aligned
         // warp-collective, so the O round trip must not diverge across rows.
@@ -453,7 +457,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           m_ref = m_new;
         }
         uint32_t pk[kBN / 2];
-        float rs = 0.f;
+        float rsp[4] = {0.f, 0.f, 0.f, 0.f};              // 4 independent row-sum chains
         const float sc = p.scale_log2, nm = -m_ref;
         if (full) {
           // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
@@ -463,18 +467,18 @@ __global__ void __launch_bounds__(kExtThreads, 1)
             const float x0 = fmaf(sv[2 * c], sc, nm), x1 = fmaf(sv[2 * c + 1], sc, nm);
             const float e0 = fast_exp2(x0);
             const float e1 = (c & 1) ? exp2_poly3(x1) : fast_exp2(x1);
-            rs += e0 + e1;
+            rsp[c & 3] += e0 + e1;
             pk[c] = pack_bf16(e0, e1);
           }
         } else {
 #pragma unroll
           for (int c = 0; c < kBN / 2; ++c) {
             const float e0 = fast_exp2(fmaf(sv[2 * c], sc, nm)), e1 = fast_exp2(fmaf(sv[2 * c + 1], sc, nm));
-            rs += e0 + e1;
+            rsp[c & 3] += e0 + e1;
             pk[c] = pack_bf16(e0, e1);
           }
         }
-        l += rs;
+        l += (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
         tmem_st32(t_s, pk);
         tmem_st32(t_s + 32, pk + 32);
         tmem_st_wait();
