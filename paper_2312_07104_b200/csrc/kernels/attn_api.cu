@@ -216,6 +216,7 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   ep.part_splits = pl.total_splits;
   ep.part_base = 0;
   ep.cas_prefix = shared_len;
+  ep.pdl = rx::pdl_on();
   e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, batch, st);
   if (e != cudaSuccess) return RX_E_CUDA;
   // (3) log-sum-exp merge of shared + suffix partials

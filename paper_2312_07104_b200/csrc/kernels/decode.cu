@@ -354,6 +354,7 @@ static bool pdl_enabled() {
   }
   return v != 0;
 }
+int pdl_on() { return pdl_enabled() ? 1 : 0; }
 
 template <typename Kern, typename... Args>
 static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
@@ -414,9 +415,10 @@ cudaError_t launch_decode_multi(int head_dim, int G, const DecodeParams& p, int 
 }
 
 cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st) {
-  if (head_dim == 64) decode_merge_kernel<64><<<merge_grid(batch, p.h_q), kMergeWarps * 32, 0, st>>>(p, batch);
-  else decode_merge_kernel<128><<<merge_grid(batch, p.h_q), kMergeWarps * 32, 0, st>>>(p, batch);
-  return cudaPeekAtLastError();
+  // PDL: the merge waits (griddepcontrol.wait) for the preceding grid before reading partials
+  if (head_dim == 64)
+    return launch_pdl(decode_merge_kernel<64>, merge_grid(batch, p.h_q), dim3(kMergeWarps * 32), 0, st, p, batch);
+  return launch_pdl(decode_merge_kernel<128>, merge_grid(batch, p.h_q), dim3(kMergeWarps * 32), 0, st, p, batch);
 }
 
 // Pipeline depth per warp for head_dim 128: 2 (default: 64 KB smem, 3 CTAs/SM;

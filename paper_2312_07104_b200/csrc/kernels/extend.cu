@@ -567,6 +567,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (p.pdl && threadIdx.x == 0) pdl_wait();   // see ExtendParams::pdl
   if (threadIdx.x == 0) {   // every fetch of this CTA is done: the last CTA resets the scheduler
     __threadfence();
     if (atomicAdd(&rx_ext_sched[1], 1) == int(gridDim.x) - 1) {
@@ -661,6 +662,19 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = int(items < sms ? items : sms);   // persistent: one CTA per SM
+  if (p.pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kExtThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, extend_kernel<HD, G>, pp, mp);
+  }
   extend_kernel<HD, G><<<grid, kExtThreads, C::SMEM, st>>>(pp, mp);
   return cudaPeekAtLastError();
 }

@@ -82,6 +82,11 @@ struct ExtendParams {
   int part_base;
   int cas_prefix;               // shared prefix length (cascade mode; prefix_lens unused)
   int trace;                    // development timeline tracer (RX_EXT_TRACE)
+  // cascade partials launched as a programmatic dependent of the suffix decode: the grid may
+  // start before that decode completes (it reads only the shared prefix and writes disjoint
+  // partials); one thread per CTA waits for it before exiting, so the merge that waits on this
+  // grid also sees the decode's partials
+  int pdl;
 };
 
 struct DecodePlan {
@@ -161,6 +166,7 @@ cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32
                                 const int32_t* prefix, const int32_t* rows, const int32_t* rtt, int64_t rtt_stride,
                                 const void* k, const void* v, void* kpool, void* vpool, cudaStream_t st);
 cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st);
+int pdl_on();   // RX_PDL knob (decode.cu)
 cudaError_t launch_extend_cascade(int head_dim, int G, const ExtendParams& p, const void* q, int batch,
                                   cudaStream_t st);
 cudaError_t launch_decode(int head_dim, int G, const DecodeParams& p, int batch, cudaStream_t st, int* launches);
