@@ -152,8 +152,12 @@ struct rx_cache {
 
 namespace {
 
+// Length of the common prefix: 64-token blocks by memcmp (vectorised by libc; long shared
+// prefixes such as an 8 k-token RAG context are walked at memory speed), then token by token.
 inline size_t common_len(const int32_t* a, size_t na, const int32_t* b, size_t nb) {
   size_t n = na < nb ? na : nb, k = 0;
+  constexpr size_t kBlk = 64;
+  while (k + kBlk <= n && std::memcmp(a + k, b + k, kBlk * sizeof(int32_t)) == 0) k += kBlk;
   while (k < n && a[k] == b[k]) ++k;
   return k;
 }
@@ -242,8 +246,9 @@ rx_status rx_insert(rx_cache* c, const int32_t* tokens, const int32_t* slots, in
     size_t k = common_len(ch->tokens.data(), ch->tokens.size(), tokens + i, size_t(n - i));
     if (k < ch->tokens.size()) ch = c->split(ch, k);
     ch->last_access = now;
-    for (size_t j = 0; j < k; ++j)
-      if (slots[i + j] != ch->slots[j]) dup.push_back(slots[i + j]);  // R10
+    if (std::memcmp(slots + i, ch->slots.data(), k * sizeof(int32_t)) != 0)   // R10 (usually equal)
+      for (size_t j = 0; j < k; ++j)
+        if (slots[i + j] != ch->slots[j]) dup.push_back(slots[i + j]);
     i += int64_t(k);
     cur = ch;
   }
