@@ -398,10 +398,17 @@ rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch,
  * device), rtt[row_b][seq_len[b] - 1] = new_slots[b] is recorded, and the
  * query attends over positions 0 .. seq_len[b]-1 including the new token.
  * Equivalent to rx_store_kv(...) followed by rx_decode(...), in one kernel
- * (plus the split merge).  d_rtt is written (one entry per request). */
+ * (plus the split merge).  d_rtt is written (one entry per request).
+ * d_stable_lens (int32 [batch], device, nullable): positions < stable_lens[b]
+ * of request b were written by work that completed before the previous
+ * rx_decode* call on the stream was launched (e.g. the prompt, stored by the
+ * batch's rx_extend).  The kernels are launched as programmatic dependents of
+ * the previous step: they read those positions while the previous step still
+ * drains and wait for it before anything else (the newest generated
+ * positions, the split workspace, the append).  null: wait first. */
 rx_status rx_decode_append(const rx_attn_cfg* cfg, int32_t batch,
                            int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
-                           const int32_t* d_seq_lens, int32_t max_seq_len,
+                           const int32_t* d_seq_lens, const int32_t* d_stable_lens, int32_t max_seq_len,
                            const void* d_q, const void* d_k_new, const void* d_v_new,
                            const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
                            int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream);
@@ -421,7 +428,8 @@ size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t 
  * Workspace: rx_decode_cascade_workspace_bytes(cfg, batch, max_seq_len, shared_len). */
 rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch,
                                    int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
-                                   const int32_t* d_seq_lens, int32_t max_seq_len, int32_t shared_len,
+                                   const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                                   int32_t max_seq_len, int32_t shared_len,
                                    const void* d_q, const void* d_k_new, const void* d_v_new,
                                    const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
                                    int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream);

@@ -82,11 +82,11 @@ SIGNATURES = {
                                     vp, vp, vp, vp, vp, i64, vp, vp, sz, vp]),
     "rx_extend_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i64, i32]),
     "rx_decode": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, i64, vp, vp, sz, vp]),
-    "rx_decode_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, i64,
+    "rx_decode_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, i64,
                                    vp, vp, sz, vp]),
     "rx_decode_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32]),
-    "rx_decode_cascade_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, i32, i32, vp, vp, vp, vp, vp,
-                                           vp, i64, vp, vp, sz, vp]),
+    "rx_decode_cascade_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, i32, i32, vp, vp, vp, vp,
+                                           vp, vp, i64, vp, vp, sz, vp]),
     "rx_decode_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32, i32]),
     "rx_last_launch_count": (i32, []),
 }

@@ -398,13 +398,14 @@ def rx_decode(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int, q, k_pool, v_
 
 
 def rx_decode_append(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int, q, k_new, v_new, new_slots, k_pool,
-                     v_pool, o, ws=None, stream=None):
+                     v_pool, o, ws=None, stream=None, stable_lens=None):
     """rx_store_kv + rtt append + rx_decode of one decode step, in one kernel (include/rx.h)."""
     import torch
     batch = seq_lens.shape[0]
     ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
     st = lib.rx_decode_append(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
-                              _dev(rows, torch.int32, "rows"), _dev(seq_lens, torch.int32, "seq_lens"), max_seq_len,
+                              _dev(rows, torch.int32, "rows"), _dev(seq_lens, torch.int32, "seq_lens"),
+                              _dev(stable_lens, torch.int32, "stable_lens"), max_seq_len,
                               _dev(q, torch.bfloat16, "q"), _dev(k_new, torch.bfloat16, "k_new"),
                               _dev(v_new, torch.bfloat16, "v_new"), _dev(new_slots, torch.int32, "new_slots"),
                               _dev(k_pool, torch.bfloat16, "k_pool"), _dev(v_pool, torch.bfloat16, "v_pool"),
@@ -418,14 +419,15 @@ def rx_decode_cascade_workspace_bytes(cfg: AttnCfg, batch: int, max_seq_len: int
 
 
 def rx_decode_cascade_append(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int, shared_len: int, q, k_new, v_new,
-                             new_slots, k_pool, v_pool, o, ws=None, stream=None):
+                             new_slots, k_pool, v_pool, o, ws=None, stream=None, stable_lens=None):
     """Shared-prefix decode step (include/rx.h rx_decode_cascade_append)."""
     import torch
     batch = seq_lens.shape[0]
     ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
     st = lib.rx_decode_cascade_append(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
                                       _dev(rows, torch.int32, "rows"), _dev(seq_lens, torch.int32, "seq_lens"),
-                                      max_seq_len, shared_len, _dev(q, torch.bfloat16, "q"),
+                                      _dev(stable_lens, torch.int32, "stable_lens"), max_seq_len, shared_len,
+                                      _dev(q, torch.bfloat16, "q"),
                                       _dev(k_new, torch.bfloat16, "k_new"), _dev(v_new, torch.bfloat16, "v_new"),
                                       _dev(new_slots, torch.int32, "new_slots"), _dev(k_pool, torch.bfloat16, "k_pool"),
                                       _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0],

@@ -81,7 +81,7 @@ static rx_status decode_impl(const rx_attn_cfg* cfg, int32_t batch, const int32_
                              const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
                              const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
                              size_t ws_bytes, void* stream, const void* d_k_new, const void* d_v_new,
-                             const int32_t* d_new_slots, int32_t* d_rtt_w) {
+                             const int32_t* d_new_slots, int32_t* d_rtt_w, const int32_t* d_stable_lens) {
   rx_status s = check_cfg(cfg);
   if (s != RX_OK) return s;
   if (batch < 0 || max_seq_len < 0 || num_slots < 1) return RX_E_INVALID;
@@ -113,6 +113,7 @@ static rx_status decode_impl(const rx_attn_cfg* cfg, int32_t batch, const int32_
   p.v_new = static_cast<const __nv_bfloat16*>(d_v_new);
   p.new_slots = d_new_slots;
   p.rtt_w = d_rtt_w;
+  p.stable_lens = d_stable_lens;
   int launches = 0;
   cudaError_t e = rx::launch_decode(cfg->head_dim, cfg->h_q / cfg->h_kv, p, batch,
                                     static_cast<cudaStream_t>(stream), &launches);
@@ -126,16 +127,17 @@ rx_status rx_decode(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
                     const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
                     size_t ws_bytes, void* stream) {
   return decode_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_pool, d_v_pool,
-                     num_slots, d_o, d_ws, ws_bytes, stream, nullptr, nullptr, nullptr, nullptr);
+                     num_slots, d_o, d_ws, ws_bytes, stream, nullptr, nullptr, nullptr, nullptr, nullptr);
 }
 
 rx_status rx_decode_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
-                           const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
-                           const void* d_k_new, const void* d_v_new, const int32_t* d_new_slots, void* d_k_pool,
-                           void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
+                           const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                           int32_t max_seq_len, const void* d_q, const void* d_k_new, const void* d_v_new,
+                           const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* d_o,
+                           void* d_ws, size_t ws_bytes, void* stream) {
   if (!d_k_new || !d_v_new || !d_new_slots) return RX_E_INVALID;
   return decode_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_pool, d_v_pool,
-                     num_slots, d_o, d_ws, ws_bytes, stream, d_k_new, d_v_new, d_new_slots, d_rtt);
+                     num_slots, d_o, d_ws, ws_bytes, stream, d_k_new, d_v_new, d_new_slots, d_rtt, d_stable_lens);
 }
 
 size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len,
@@ -145,7 +147,8 @@ size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, 
 }
 
 rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
-                                   const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len,
+                                   const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                                   int32_t max_seq_len,
                                    int32_t shared_len, const void* d_q, const void* d_k_new, const void* d_v_new,
                                    const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool, int64_t num_slots,
                                    void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
@@ -155,8 +158,9 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   g_last_launches = 0;
   if (batch == 0) return RX_OK;
   if (shared_len == 0)   // nothing shared: the ordinary fused path
-    return rx_decode_append(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_new, d_v_new,
-                            d_new_slots, d_k_pool, d_v_pool, num_slots, d_o, d_ws, ws_bytes, stream);
+    return rx_decode_append(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, d_stable_lens, max_seq_len, d_q,
+                            d_k_new, d_v_new, d_new_slots, d_k_pool, d_v_pool, num_slots, d_o, d_ws, ws_bytes,
+                            stream);
   if (max_seq_len <= shared_len || !d_rtt || !d_seq_lens || !d_q || !d_k_new || !d_v_new || !d_new_slots ||
       !d_k_pool || !d_v_pool || !d_o || rtt_stride < max_seq_len)
     return RX_E_INVALID;
@@ -193,6 +197,7 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   dp.rtt_w = d_rtt;
   dp.kv_start = shared_len;
   dp.split_base = pl.n_sh;
+  dp.stable_lens = d_stable_lens;
   int launches = 0;
   cudaError_t e = rx::launch_decode(cfg->head_dim, G, dp, batch, st, &launches);
   if (e != cudaSuccess) return RX_E_CUDA;

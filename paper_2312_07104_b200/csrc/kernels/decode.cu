@@ -48,9 +48,14 @@ struct DecCfg {
   static_assert(SMEM >= kDecWarps * HD * 8 * 4, "merge scratch must fit");
 };
 
+// slot > 0: pool row; slot == kNewTok: the step's own new token, read from the k_new / v_new
+// argument rows (knew / vnew, this head) — so no CTA has to wait for the pool append; else zeros
+constexpr int kNewTok = -2;
+
 template <int HD>
 __device__ __forceinline__ void dec_issue_block(uint32_t kdst, uint32_t vdst, const __nv_bfloat16* kpool,
-                                                const __nv_bfloat16* vpool, int slot, int h_kv, int g) {
+                                                const __nv_bfloat16* vpool, int slot, int h_kv, int g,
+                                                const __nv_bfloat16* knew, const __nv_bfloat16* vnew) {
   constexpr int CPR = HD / 8;  // chunks per row
   const int lane = lane_id();
 #pragma unroll
@@ -58,11 +63,11 @@ __device__ __forceinline__ void dec_issue_block(uint32_t kdst, uint32_t vdst, co
     const int idx = c * 32 + lane;
     const int r = idx / CPR, ch = idx % CPR;
     const int sl = __shfl_sync(0xffffffffu, slot, r);
-    const bool ok = sl > 0;
-    const int64_t off = (int64_t(ok ? sl : 0) * h_kv + g) * HD + ch * 8;
+    const bool ok = sl > 0 || sl == kNewTok;
+    const int64_t off = (int64_t(sl > 0 ? sl : 0) * h_kv + g) * HD + ch * 8;
     const uint32_t so = r * DecCfg<HD>::RB + ((ch ^ (r & 7)) << 4);
-    cp_async_16(kdst + so, kpool + off, ok ? 16u : 0u);
-    cp_async_16(vdst + so, vpool + off, ok ? 16u : 0u);
+    cp_async_16(kdst + so, sl == kNewTok ? knew + ch * 8 : kpool + off, ok ? 16u : 0u);
+    cp_async_16(vdst + so, sl == kNewTok ? vnew + ch * 8 : vpool + off, ok ? 16u : 0u);
   }
 }
 
@@ -84,29 +89,29 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   const int row = p.rows ? p.rows[b] : b;
   const int32_t* slots = p.rtt + int64_t(row) * p.rtt_stride;
 
-  // Decode-append (rx_decode_append): the newest token's KV arrives with the
-  // call.  The last split of each (request, kv head) stores that head's row
-  // into the pool slot (A5) and, for kv head 0, appends the slot to the
-  // req_to_token row (A4); position L-1 then reads its slot from the argument,
-  // never from the table, so no CTA races the table write.
-  // PDL (launch_decode): nothing below may read the pool, the table or the workspace before the
-  // preceding grid (the previous step's decode / merge) has completed
-  pdl_wait();
+  // Decode-append (rx_decode_append): the newest token's KV arrives with the call.  Position L-1
+  // is read from the k_new / v_new argument (kNewTok), and the last split of each (request, kv
+  // head) stores that head's row into the pool slot (A5) — for kv head 0 also the slot into the
+  // req_to_token row (A4) — at the END, after the dependency wait below.
   const bool append = !MULTI && p.new_slots != nullptr;
   const int new_slot = append ? p.new_slots[b] : 0;
-  if (append && s == nsplit - 1) {
-    constexpr int VPR = HD / 8;                      // 16-byte vectors per head row
-    const int64_t src = (int64_t(b) * p.h_kv + g) * HD;
-    const int64_t dst = (int64_t(new_slot) * p.h_kv + g) * HD;
-    if (threadIdx.x < VPR)
-      reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.kpool) + dst)[threadIdx.x] =
-          reinterpret_cast<const uint4*>(p.k_new + src)[threadIdx.x];
-    else if (threadIdx.x < 2 * VPR)
-      reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.vpool) + dst)[threadIdx.x - VPR] =
-          reinterpret_cast<const uint4*>(p.v_new + src)[threadIdx.x - VPR];
-    if (g == 0 && threadIdx.x == 2 * VPR) p.rtt_w[int64_t(row) * p.rtt_stride + L - 1] = new_slot;
-    __syncthreads();  // the row is in L2 before this CTA's cp.async gathers read it
-  }
+  const __nv_bfloat16* knew_row = append ? p.k_new + (int64_t(b) * p.h_kv + g) * HD : nullptr;
+  const __nv_bfloat16* vnew_row = append ? p.v_new + (int64_t(b) * p.h_kv + g) * HD : nullptr;
+  // Programmatic dependent launch (launch_decode): this grid may start while the previous decode
+  // step / merge still runs.  Positions < stable (written by plain-launched kernels before the
+  // decode phase: the prompt) are read at once; everything the previous steps wrote — table
+  // entries and K/V of generated positions, the split workspace the previous merge reads — only
+  // after griddepcontrol.wait.  stable_lens null: wait before anything.
+  const int stable = (MULTI || !p.stable_lens) ? 0 : min(p.stable_lens[b], L - 1);
+  bool waited = false;
+  auto dep_wait = [&]() {
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
+  };
+  if (stable <= start) dep_wait();
+  pdl_launch_dependents();   // every CTA has started: the next step may be scheduled
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
@@ -136,16 +141,19 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   const int nblk = (end - start + kBlk - 1) / kBlk;
   const int my = warp < nblk ? (nblk - warp + kDecWarps - 1) / kDecWarps : 0;
   auto tok0 = [&](int i) { return start + (warp + i * kDecWarps) * kBlk; };
+  // block i is late if it holds a position >= stable: wait (whole warp) before its table reads
+  auto late = [&](int i) { return i < my && tok0(i) + kBlk > stable; };
   auto load_slot = [&](int i) -> int {
+    if (late(i)) dep_wait();
     if (i >= my || lane >= kBlk) return 0;
     const int t = tok0(i) + lane;
-    return t < end ? ((append && t == L - 1) ? new_slot : slots[t]) : 0;
+    return t < end ? ((append && t == L - 1) ? kNewTok : slots[t]) : 0;
   };
 
 #pragma unroll
   for (int st = 0; st < C::STAGES - 1; ++st) {
     const int sl = load_slot(st);
-    if (st < my) dec_issue_block<HD>(kst(st), vst(st), p.kpool, p.vpool, sl, p.h_kv, g);
+    if (st < my) dec_issue_block<HD>(kst(st), vst(st), p.kpool, p.vpool, sl, p.h_kv, g, knew_row, vnew_row);
     cp_async_commit();
   }
   int slot_pref = load_slot(C::STAGES - 1);
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
     {
       const int ii = i + C::STAGES - 1;
       if (ii < my) dec_issue_block<HD>(kst(ii % C::STAGES), vst(ii % C::STAGES), p.kpool, p.vpool, slot_pref,
-                                       p.h_kv, g);
+                                       p.h_kv, g, knew_row, vnew_row);
       cp_async_commit();
       slot_pref = load_slot(i + C::STAGES);
     }
@@ -233,7 +241,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
     __syncwarp();
   }
   cp_async_wait<0>();
-  pdl_launch_dependents();   // this CTA's streaming is done: let the next grid's CTAs fill the SM
+  dep_wait();   // before writing the output / split workspace and the pool append
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -292,6 +300,19 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
       if (d == 0) p.ws_lse[base] = M + __log2f(Ls);
     }
   }
+  if (append && s == nsplit - 1) {
+    // A5 + A4 of this step (after the dependency wait: the slot may have been freed by a request
+    // that finished at the previous step, whose kernel could otherwise still be reading it)
+    constexpr int VPR = HD / 8;                      // 16-byte vectors per head row
+    const int64_t dst = (int64_t(new_slot) * p.h_kv + g) * HD;
+    if (threadIdx.x < VPR)
+      reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.kpool) + dst)[threadIdx.x] =
+          reinterpret_cast<const uint4*>(knew_row)[threadIdx.x];
+    else if (threadIdx.x < 2 * VPR)
+      reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.vpool) + dst)[threadIdx.x - VPR] =
+          reinterpret_cast<const uint4*>(vnew_row)[threadIdx.x - VPR];
+    if (g == 0 && threadIdx.x == 2 * VPR) p.rtt_w[int64_t(row) * p.rtt_stride + L - 1] = new_slot;
+  }
 }
 
 // Log-sum-exp merge of split partials (A8): o = sum_s 2^(lse_s - LSE) o_s.
@@ -301,8 +322,9 @@ constexpr int kMergeWarps = 8;
 
 template <int HD>
 __global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const DecodeParams p, int rows) {
+  pdl_launch_dependents();   // the next step may be scheduled now: it reads only stable positions
+                             // before its own wait (which covers this merge)
   pdl_wait();                // the partials of the preceding grid(s) are complete
-  pdl_launch_dependents();   // ... so the next step may start (it waits for this merge in turn)
   const int lane = threadIdx.x & 31;
   const int64_t pair = int64_t(blockIdx.x) * kMergeWarps + (threadIdx.x >> 5);
   if (pair >= int64_t(rows) * p.h_q) return;

@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       }
       // epilogue: O[qb] complete once this item's last P.V landed
       mbar_wait(o_ready + qb, (it >> 1) & 1);
+      if (p.pdl) pdl_wait();   // cascade partials: the previous step's merge must be done reading them
       if (threadIdx.x == 128) ext_trace(p.trace, 9, it);
       tc_fence_after();
       const uint32_t t_o = tmem + lane_off + C::O_COL + qb * HD;

@@ -38,6 +38,9 @@ struct DecodeParams {
   // the split_base shared partials); the merge combines split_base + nsplit_b.
   int kv_start;
   int split_base;
+  // nullable: positions < stable_lens[b] were written before the decode phase (by plain-launched
+  // kernels) and may be read before the programmatic-dependency wait
+  const int32_t* stable_lens;
   // multi-query mode (rx_extend with short segments, decode_kernel<..., MULTI>): request b owns
   // query rows qo_indptr[b] .. qo_indptr[b+1] (q / o ragged [N, h_q, HD]) at positions
   // prefix_lens[b] + j; causal inside the segment; CTA z = b * col_tiles + tile of 8 columns
@@ -83,9 +86,9 @@ struct ExtendParams {
   int cas_prefix;               // shared prefix length (cascade mode; prefix_lens unused)
   int trace;                    // development timeline tracer (RX_EXT_TRACE)
   // cascade partials launched as a programmatic dependent of the suffix decode: the grid may
-  // start before that decode completes (it reads only the shared prefix and writes disjoint
-  // partials); one thread per CTA waits for it before exiting, so the merge that waits on this
-  // grid also sees the decode's partials
+  // start before that decode completes (it reads only the shared prefix); its epilogue waits for
+  // the decode (hence the previous step's merge) before writing partials, and one thread per CTA
+  // waits before exiting, so the merge that waits on this grid also sees the decode's partials
   int pdl;
 };
 

@@ -363,6 +363,9 @@ class Engine:
         if self._shared < self.cascade_min_len:
             self._shared = 0
         self._extend(rs, slots, prefix, ext)
+        # positions every later decode step may read before its programmatic-dependency wait:
+        # those written by this batch's prefill (plain launches, complete before the first step)
+        self._stable = (n_prompt + first).astype(np.int32)
         t0 = time.perf_counter()
         nseg = np.array([len(r.segs) for r in rs], dtype=np.int64)
         self._finish_many(rs, np.nonzero(nseg == 0)[0], slots)
@@ -592,7 +595,7 @@ class Engine:
         then one rx_decode_append (or rx_decode_cascade_append) per step."""
         dev = self.device
         offs = np.zeros(len(steps) + 1, dtype=np.int64)
-        offs[1:] = np.cumsum([3 * len(r) for r, _, _ in steps])
+        offs[1:] = np.cumsum([4 * len(r) for r, _, _ in steps])
         name = f"dec{self._ring % 4}"
         self._ring += 1
         stage = self._pinned(name, int(offs[-1]))
@@ -604,6 +607,7 @@ class Engine:
             sn[o0:o0 + B] = new
             sn[o0 + B:o0 + 2 * B] = pos + 1             # seq_len counts the new token
             sn[o0 + 2 * B:o0 + 3 * B] = running         # table row of each running request
+            sn[o0 + 3 * B:o0 + 4 * B] = self._stable[running]   # written by the batch's prefill
             ms = int(pos.max()) + 1
             need = max(need, api.rx_decode_cascade_workspace_bytes(self.cfg, B, ms, sh) if sh
                        else api.rx_decode_workspace_bytes(self.cfg, B, ms))
@@ -621,16 +625,16 @@ class Engine:
             B = len(running)
             q, k, v = self.bank.dec[self._dec_i]
             self._dec_i += 1
-            d = d_all[o0:o0 + 3 * B]
+            d = d_all[o0:o0 + 4 * B]
             max_seq = int(pos.max()) + 1
             o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
             ev0 = self._tbeg() if per_call else None
             if sh:
-                api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, sh, q, k, v,
-                                             d[:B], self.k_pool, self.v_pool, o, self._ws)
+                api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, sh, q, k, v,
+                                             d[:B], self.k_pool, self.v_pool, o, self._ws, stable_lens=d[3 * B:])
             else:
-                api.rx_decode_append(self.cfg, self._rtt, d[2 * B:], d[B:2 * B], max_seq, q, k, v, d[:B],
-                                     self.k_pool, self.v_pool, o, self._ws)
+                api.rx_decode_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, q, k, v, d[:B],
+                                     self.k_pool, self.v_pool, o, self._ws, stable_lens=d[3 * B:])
             nl = api.rx_last_launch_count()
             self.stats["launches"] += nl
             # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot indices,

@@ -213,3 +213,20 @@ def test_host_io_path_bitwise_equal():
         assert len(ref) == len(sink.out)
         for a, b in zip(ref, sink.out):
             assert torch.equal(a.view(-1), b.view(-1))
+
+
+def test_duplicate_slots_freed_and_reused_mid_phase():
+    """Requests with the SAME uncached prompt in one batch (no hint): each computes the prompt; the
+    first to finish caches it and every later finisher frees its duplicate slots (R10), which the
+    next decode step reallocates at once (smallest free first, R8) while the previous step's
+    kernel may still be draining (programmatic dependent launch): the append into a reused slot
+    must come after the dependency wait.  Every row vs the oracle, trace bit-exact."""
+    from rxgen.workloads import Request, Workload, Shape
+    rng = np.random.default_rng(11)
+    prompt = rng.integers(1, 30000, 300).astype(np.int32)
+    reqs = [Request(prompt.copy(), n, f"d{n}") for n in (1, 2, 3, 5, 8, 13, 21, 34)]
+    wl = Workload("DUP", Shape(32, 8, 128), 4096, 32000, 11, [("batch", reqs)])
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, _all_ext, _all_dec)
+    assert oe.trace == e.trace
+    assert any(t[0] == "insert" and t[3] > 0 for t in e.trace)      # duplicates were freed
