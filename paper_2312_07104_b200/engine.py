@@ -356,8 +356,11 @@ class Engine:
         # decode steps attend it once for the whole batch (rx_decode_cascade_append)
         mp = int(prefix.min())
         if self.cascade and B >= self.cascade_min_batch and mp >= self.cascade_min_len:
-            diff = np.nonzero((slots[:, :mp] != slots[0:1, :mp]).any(axis=0))[0]
-            self._shared = int(diff[0]) if len(diff) else mp
+            if all(r.node == rs[0].node for r in rs):
+                self._shared = mp            # one matched radix node: identical slots up to its depth
+            else:
+                diff = np.nonzero((slots[:, :mp] != slots[0:1, :mp]).any(axis=0))[0]
+                self._shared = int(diff[0]) if len(diff) else mp
         else:
             self._shared = 0
         if self._shared < self.cascade_min_len:
@@ -439,7 +442,10 @@ class Engine:
         off = np.zeros(len(idx) + 1, dtype=np.int64)
         off[1:] = np.cumsum(lens)
         toks = np.concatenate([rs[b].tokens[:n] for b, n in zip(idx, lens)])
-        sl = np.concatenate([slots[b, :n] for b, n in zip(idx, lens)])
+        if (lens == lens[0]).all():
+            sl = slots[idx, :int(lens[0])].reshape(-1)
+        else:
+            sl = np.concatenate([slots[b, :n] for b, n in zip(idx, lens)])
         d, nc, nd = self.cache.rx_finish_batch([rs[b].node for b in idx], toks, off, sl)
         if self.record:
             for i, b in enumerate(idx):
