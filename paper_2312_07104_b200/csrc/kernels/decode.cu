@@ -111,7 +111,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
     }
   };
   if (stable <= start) dep_wait();
-  pdl_launch_dependents();   // every CTA has started: the next step may be scheduled
+  // with a stable region the next step is released as soon as every CTA has started (it reads only
+  // its own stable positions before its wait); without one, after this CTA's streaming (the old
+  // schedule: the cascade chain's tcgen05 partial kernel needs whole SMs and must not be delayed)
+  const bool early_trigger = !MULTI && p.stable_lens != nullptr;
+  if (early_trigger) pdl_launch_dependents();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
@@ -242,6 +246,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   }
   cp_async_wait<0>();
   dep_wait();   // before writing the output / split workspace and the pool append
+  if (!early_trigger) pdl_launch_dependents();
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);

@@ -511,7 +511,6 @@ class Engine:
             d_new = dstage[o2 + 2 * total:o2 + 3 * total]
         else:
             self._rtt = dstage[hdr:].view(R, stride)
-        self._B = R
         ws_n = api.rx_decode_workspace_bytes(self.cfg, R, stride)
         if self._ws is None or self._ws.numel() < ws_n:
             self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
@@ -636,8 +635,10 @@ class Engine:
             o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
             ev0 = self._tbeg() if per_call else None
             if sh:
+                # (no stable region: in the cascade chain the early release measured slower, C5 step
+                # 101 -> 140 us, because the tcgen05 shared-prefix kernel needs whole SMs)
                 api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, sh, q, k, v,
-                                             d[:B], self.k_pool, self.v_pool, o, self._ws, stable_lens=d[3 * B:])
+                                             d[:B], self.k_pool, self.v_pool, o, self._ws)
             else:
                 api.rx_decode_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, q, k, v, d[:B],
                                      self.k_pool, self.v_pool, o, self._ws, stable_lens=d[3 * B:])
@@ -660,19 +661,19 @@ class Engine:
 
     # ------------------------------------------------------------------ pinned staging
     def _pinned(self, name, n):
-        """Pinned int32 staging buffer of >= n elements from a pool: any buffer whose last H2D copy
-        has completed is reused (smallest that fits), so steady state allocates nothing — pinned
-        allocation (cudaHostAlloc) takes milliseconds.  `name` tags the checkout for _pinned_done."""
-        pool = self._pin_pool
-        best = None
+        """Pinned int32 staging buffer of >= n elements from a pool: the oldest buffer that is large
+        enough and whose last H2D copy has completed is reused, so steady state allocates nothing —
+        pinned allocation (cudaHostAlloc) takes milliseconds.  `name` tags the checkout."""
+        pool = self._pin_pool                 # oldest first: the first entries are the ones done
+        pick = None
         for i, (buf, ev) in enumerate(pool):
-            if buf.numel() >= n and (ev is None or ev.query()):
-                if best is None or buf.numel() < pool[best][0].numel():
-                    best = i
-        if best is None:
+            if buf.numel() >= n and ev.query():
+                pick = i
+                break
+        if pick is None:
             buf = torch.empty(max(n, 1 << 16), dtype=torch.int32, pin_memory=True)
         else:
-            buf, _ = pool.pop(best)
+            buf, _ = pool.pop(pick)
         self._pin_cache[name] = buf
         return buf[:n]
 

@@ -47,9 +47,13 @@ def main():
     ei = 0
     dec_ms, dec_n, dec_bytes = 0.0, 0, 0.0
     kern_ms = 0.0
+    prev_end = s
     for kind, ev0, ev1, work, nl, calls in eng.timer:
         ms = ev0.elapsed_time(ev1)
         kern_ms += ms
+        if kind == "extend":
+            print(f"  (gap before this extend: {prev_end.elapsed_time(ev0):.3f} ms)")
+        prev_end = ev1
         if kind == "extend":
             meta = ext_calls[ei].meta
             ei += 1
