@@ -356,7 +356,9 @@ class Engine:
         # decode steps attend it once for the whole batch (rx_decode_cascade_append)
         mp = int(prefix.min())
         if self.cascade and B >= self.cascade_min_batch and mp >= self.cascade_min_len:
-            if all(r.node == rs[0].node for r in rs):
+            if (slots[:, 0] != slots[0, 0]).any():
+                self._shared = 0             # rows differ at position 0: nothing shared (e.g. C3 sessions)
+            elif all(r.node == rs[0].node for r in rs):
                 self._shared = mp            # one matched radix node: identical slots up to its depth
             else:
                 diff = np.nonzero((slots[:, :mp] != slots[0:1, :mp]).any(axis=0))[0]
