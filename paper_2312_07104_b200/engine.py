@@ -385,9 +385,14 @@ class Engine:
         cur = n_prompt + first
         step = 0
         steps = []
+        # plain decoding (every segment one token): no per-request Python per step
+        unit = all(r.first == 0 and (len(r.segs) == 0 or int(r.segs.max()) == 1) for r in rs)
         while len(running):
             t0 = time.perf_counter()
-            lens = np.array([rs[b].segs[step] for b in running], dtype=np.int64)
+            if unit:
+                lens = np.ones(len(running), dtype=np.int64)
+            else:
+                lens = np.array([rs[b].segs[step] for b in running], dtype=np.int64)
             new = self._alloc(int(lens.sum()))
             pos = cur[running].copy()
             if (lens == 1).all():
