@@ -88,3 +88,14 @@ def test_c4_admission_waves_and_eviction():
     admits = [t for t in o if t[0] == "admit"]
     assert len(admits) > 3 and sum(t[0] == "evict" for t in o) > 0
     _cmp(o, e)
+
+
+def test_ragged_flat_matches_loop():
+    from paper_2312_07104_b200.engine import _ragged_flat
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        n = int(rng.integers(0, 12))
+        starts = rng.integers(0, 1000, n)
+        lens = rng.integers(0, 9, n)
+        ref = np.concatenate([np.arange(s, s + l) for s, l in zip(starts, lens)]) if n else np.zeros(0)
+        assert np.array_equal(_ragged_flat(starts, lens), ref.astype(np.int64))
