@@ -304,6 +304,23 @@ int64_t rx_router_dump_json(const rx_router* r, char* buf, int64_t cap);
  *             position p of the request in that row (D10 in SURVEY §2).
  *   d_rows    int32 [batch] or null: batch entry b uses rtt row d_rows[b]
  *             (null: row b), so a persistent table is never re-uploaded.
+ *
+ * Streams and concurrency.  Every device call is asynchronous on the given
+ * stream (a cudaStream_t; null = the legacy default stream) and returns after
+ * enqueueing its launches; faults surface at the caller's next synchronisation.
+ * Calls on DIFFERENT streams may run concurrently on one device provided they
+ * use different workspaces and do not write the same pool slots, table rows or
+ * outputs.  The library holds no device state between calls: all scheduling
+ * state lives in the caller's workspace (below).  Host-side it keeps only
+ * per-device, thread-safe caches (kernel attributes, SM counts).
+ *
+ * Workspaces.  d_ws / ws_bytes is caller-owned device memory (the library never
+ * allocates device memory).  Its first 256 bytes are a header holding the
+ * persistent extend kernel's work counters: they MUST be zero before the
+ * workspace is first used (allocate it zeroed), and every call leaves them zero
+ * again; split-KV partials follow the header.  One workspace may serve any
+ * sequence of calls on one stream; concurrently running calls need one each.
+ * A call given less than its rx_*_workspace_bytes(...) returns RX_E_WORKSPACE.
  */
 typedef struct {
   int32_t h_q;
@@ -312,7 +329,9 @@ typedef struct {
   float sm_scale;
 } rx_attn_cfg;
 
-/* KV store: k_pool[slots[i]] = k[i]; v_pool[slots[i]] = v[i] for i < n
+/* KV store (A5; "the KV cache of the new tokens is stored in the pool" at the
+ * slots the allocator returned, P:494-499 [App. A.1], one token per page P:181):
+ * k_pool[slots[i]] = k[i]; v_pool[slots[i]] = v[i] for i < n
  * (bit-exact copy).  If d_rtt_index is non-null, also rtt_flat[d_rtt_index[i]]
  * = slots[i] (d_rtt must then be non-null): the decode step's "append one
  * column to req_to_token" in the same launch.  Slots must be distinct and in
@@ -345,7 +364,8 @@ rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
  * decoding (§4) — the decode kernel in multi-query mode (one mma.sync
  * column per (row, GQA head), causal per column).  Two launches either way
  * (store, attention).
- * Workspace: d_ws of ws_bytes >= rx_extend_workspace_bytes(...). */
+ * Workspace: d_ws of ws_bytes >= rx_extend_workspace_bytes(...) (the 256-byte
+ * header: the tcgen05 kernel's work counters; zero on entry, zero on exit). */
 rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch,
                     const int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,
                     const int32_t* d_prefix_lens, const int32_t* d_extend_lens,

@@ -349,8 +349,13 @@ def rx_decode_workspace_bytes(cfg: AttnCfg, batch: int, max_seq_len: int) -> int
 
 def rx_extend(cfg: AttnCfg, rtt, rows, prefix_lens, extend_lens, qo_indptr, total_new: int, max_extend_len: int,
               max_prefix_len: int, q, k_new, v_new, k_pool, v_pool, o, ws=None, stream=None):
+    """ws=None: a zeroed workspace of rx_extend_workspace_bytes is allocated (through torch) for this
+    call; callers that issue many calls pass one zero-initialised buffer (include/rx.h "Workspaces")."""
     import torch
     batch = prefix_lens.shape[0]
+    if ws is None:
+        ws = torch.zeros(max(1, rx_extend_workspace_bytes(cfg, batch, max_extend_len)), dtype=torch.uint8,
+                         device=q.device)
     ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
     st = lib.rx_extend(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
                        _dev(rows, torch.int32, "rows"), _dev(prefix_lens, torch.int32, "prefix_lens"),

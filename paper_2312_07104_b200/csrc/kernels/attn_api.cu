@@ -102,8 +102,9 @@ static rx_status decode_impl(const rx_attn_cfg* cfg, int32_t batch, const int32_
   p.rows = d_rows;
   p.seq_lens = d_seq_lens;
   const size_t n = size_t(batch) * cfg->h_q * pl.max_splits;
-  p.ws_o = static_cast<float*>(d_ws);
-  p.ws_lse = need ? reinterpret_cast<float*>(static_cast<char*>(d_ws) + n * cfg->head_dim * sizeof(float)) : nullptr;
+  char* part = need ? static_cast<char*>(d_ws) + rx::kWsHeader : nullptr;   // partials follow the header
+  p.ws_o = reinterpret_cast<float*>(part);
+  p.ws_lse = need ? reinterpret_cast<float*>(part + n * cfg->head_dim * sizeof(float)) : nullptr;
   p.h_q = cfg->h_q;
   p.h_kv = cfg->h_kv;
   p.chunk = pl.chunk;
@@ -169,8 +170,9 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   if (!d_ws || ws_bytes < need) return RX_E_WORKSPACE;
   const rx::CascadePlan pl = rx::plan_cascade(batch, cfg->h_kv, G, max_seq_len, shared_len);
   const size_t n = size_t(batch) * cfg->h_q * pl.total_splits;
-  float* ws_o = static_cast<float*>(d_ws);
-  float* ws_lse = reinterpret_cast<float*>(static_cast<char*>(d_ws) + n * cfg->head_dim * sizeof(float));
+  char* part = static_cast<char*>(d_ws) + rx::kWsHeader;
+  float* ws_o = reinterpret_cast<float*>(part);
+  float* ws_lse = reinterpret_cast<float*>(part + n * cfg->head_dim * sizeof(float));
   const float scale_log2 = cfg->sm_scale * 1.4426950408889634f;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
@@ -222,6 +224,7 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   ep.part_base = 0;
   ep.cas_prefix = shared_len;
   ep.pdl = rx::pdl_on();
+  ep.sched = static_cast<int*>(d_ws);
   e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, batch, st);
   if (e != cudaSuccess) return RX_E_CUDA;
   // (3) log-sum-exp merge of shared + suffix partials
@@ -242,7 +245,7 @@ size_t rx_extend_cascade_workspace_bytes(const rx_attn_cfg* cfg, int64_t total_n
   if (check_cfg(cfg) != RX_OK || total_new <= 0 || shared_len <= 0) return 0;
   const rx::CascadePlan pl = plan_extend_cascade(cfg, total_new, shared_len);
   const size_t n = size_t(total_new) * cfg->h_q * pl.total_splits;
-  return n * cfg->head_dim * sizeof(float) + n * sizeof(float) + 256;
+  return rx::kWsHeader + n * cfg->head_dim * sizeof(float) + n * sizeof(float) + 256;
 }
 
 rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
@@ -269,8 +272,9 @@ rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t
   g_last_launches = 0;
   const rx::CascadePlan pl = plan_extend_cascade(cfg, total_new, shared_len);
   const size_t n = size_t(total_new) * cfg->h_q * pl.total_splits;
-  float* ws_o = static_cast<float*>(d_ws);
-  float* ws_lse = reinterpret_cast<float*>(static_cast<char*>(d_ws) + n * cfg->head_dim * sizeof(float));
+  char* part = static_cast<char*>(d_ws) + rx::kWsHeader;
+  float* ws_o = reinterpret_cast<float*>(part);
+  float* ws_lse = reinterpret_cast<float*>(part + n * cfg->head_dim * sizeof(float));
   const float scale_log2 = cfg->sm_scale * 1.4426950408889634f;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // A5: the new rows into their slots
@@ -323,6 +327,7 @@ rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t
   ep.part_splits = pl.total_splits;
   ep.part_base = 0;
   ep.cas_prefix = shared_len;
+  ep.sched = static_cast<int*>(d_ws);
   e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, int(total_new), st);
   if (e != cudaSuccess) return RX_E_CUDA;
   // (3) log-sum-exp merge per row
@@ -333,10 +338,9 @@ rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t
 }
 
 size_t rx_extend_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_extend_len) {
-  (void)cfg;
-  (void)batch;
-  (void)max_extend_len;
-  return 0;
+  // the persistent kernel's work counters (the workspace header); the short-segment path uses none
+  if (check_cfg(cfg) != RX_OK || batch <= 0 || max_extend_len <= 0) return 0;
+  return rx::kWsHeader;
 }
 
 rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
@@ -344,8 +348,6 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
                     const int32_t* d_qo_indptr, int64_t total_new, int32_t max_extend_len, int32_t max_prefix_len,
                     const void* d_q, const void* d_k_new, const void* d_v_new, void* d_k_pool, void* d_v_pool,
                     int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
-  (void)d_ws;
-  (void)ws_bytes;
   rx_status s = check_cfg(cfg);
   if (s != RX_OK) return s;
   if (batch < 0 || total_new < 0 || max_extend_len < 0 || max_prefix_len < 0 || num_slots < 1)
@@ -356,6 +358,9 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
       !d_v_pool || !d_o)
     return RX_E_INVALID;
   if (rtt_stride < max_prefix_len || rtt_stride < max_extend_len) return RX_E_INVALID;
+  const int G = cfg->h_q / cfg->h_kv;
+  const bool multi = use_multi_query(G, batch, cfg->h_kv, max_extend_len);
+  if (!multi && (!d_ws || ws_bytes < rx::kWsHeader)) return RX_E_WORKSPACE;
   rx::ExtendParams p{};
   p.rtt = d_rtt;
   p.rtt_stride = rtt_stride;
@@ -372,6 +377,7 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
   p.h_kv = cfg->h_kv;
   p.num_slots = num_slots;
   p.scale_log2 = cfg->sm_scale * 1.4426950408889634f;
+  p.sched = static_cast<int*>(d_ws);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // A5: new K/V rows into their slots (independent of the attention reads:
   // new slots are never prefix slots, and the attention reads k_new/v_new)
@@ -379,8 +385,7 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt,
                                           d_prefix_lens, d_rows, d_rtt, rtt_stride, d_k_new, d_v_new, d_k_pool,
                                           d_v_pool, st);
   if (e != cudaSuccess) return RX_E_CUDA;
-  const int G = cfg->h_q / cfg->h_kv;
-  if (use_multi_query(G, batch, cfg->h_kv, max_extend_len)) {
+  if (multi) {
     // short segments (jump-forward edges, §4): (row, head) columns of the decode kernel's
     // mma.sync tile instead of 128-row tcgen05 tiles that would be almost all padding
     rx::DecodeParams dp{};

@@ -401,10 +401,9 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cud
 template <int HD, int G, int STAGES>
 static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_t st, int* launches) {
   using C = DecCfg<HD, STAGES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<HD, G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
+  {
+    cudaError_t e = ensure_smem_attr(decode_kernel<HD, G, STAGES>, C::SMEM);
+    if (e != cudaSuccess) return e;
   }
   dim3 grid(p.max_splits - p.split_base, p.h_kv, batch);   // suffix splits (cascade: shared partials come first)
   cudaError_t e = launch_pdl(decode_kernel<HD, G, STAGES>, grid, dim3(kDecWarps * 32), C::SMEM, st, p);
@@ -422,10 +421,9 @@ template <int HD, int G>
 static cudaError_t launch_decode_multi_t(const DecodeParams& p, int batch, cudaStream_t st) {
   constexpr int STG = HD == 64 ? 6 : 2;
   using C = DecCfg<HD, STG>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<HD, G, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
+  {
+    cudaError_t e = ensure_smem_attr(decode_kernel<HD, G, STG, true>, C::SMEM);
+    if (e != cudaSuccess) return e;
   }
   dim3 grid(1, p.h_kv, batch * p.col_tiles);
   decode_kernel<HD, G, STG, true><<<grid, kDecWarps * 32, C::SMEM, st>>>(p);

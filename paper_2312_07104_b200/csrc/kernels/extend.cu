@@ -60,10 +60,6 @@ constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
 // Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
 // stores clock64 per (event code, item/tile index); read back with rx_debug_ext_trace().
 __device__ unsigned long long rx_ext_trace[16 * 1024];   // [code][item & 1023]: clock64, CTA 0 only
-// Dynamic work distribution: [0] = next work index, [1] = CTAs finished.  The last CTA of a launch
-// resets both, so the next launch on the stream starts from 0 (extend launches are stream-ordered;
-// two extend kernels must not run concurrently on one device).
-__device__ int rx_ext_sched[2];
 __device__ __forceinline__ void ext_trace(int on, int code, int item) {
   if (on && blockIdx.x == 0) rx_ext_trace[code * 1024 + (item & 1023)] = clock64();   // plain store, no wait
 }
@@ -539,7 +535,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
     RingCursor c;
     for (;;) {
       int w = 0;
-      if (lane == 0) w = atomicAdd(&rx_ext_sched[0], 1);
+      if (lane == 0) w = atomicAdd(&p.sched[0], 1);
       w = __shfl_sync(0xffffffffu, w, 0);
       if (w >= W) break;
       ExtItem I;
@@ -569,11 +565,14 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
   if (p.pdl && threadIdx.x == 0) pdl_wait();   // see ExtendParams::pdl
-  if (threadIdx.x == 0) {   // every fetch of this CTA is done: the last CTA resets the scheduler
+  // Dynamic work distribution: p.sched[0] = next work index, [1] = CTAs finished, in the caller's
+  // workspace header (params.cuh kWsHeader).  Every fetch of this CTA is done: the last CTA resets
+  // both, so the workspace is zero again for the next call that uses it.
+  if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&rx_ext_sched[1], 1) == int(gridDim.x) - 1) {
-      rx_ext_sched[0] = 0;
-      rx_ext_sched[1] = 0;
+    if (atomicAdd(&p.sched[1], 1) == int(gridDim.x) - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
       __threadfence();
     }
   }
@@ -644,11 +643,11 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
     if (!make_map(&mp.kpool, p.kpool, 3, dims, str, box)) return cudaErrorInvalidValue;
     if (!make_map(&mp.vpool, p.vpool, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(extend_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
+  {
+    cudaError_t e = ensure_smem_attr(extend_kernel<HD, G>, C::SMEM);
+    if (e != cudaSuccess) return e;
   }
+  if (!p.sched) return cudaErrorInvalidValue;
   ExtendParams pp = p;
   pp.batch = batch;
   static int trace_env = -1;
@@ -656,12 +655,7 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   pp.trace = trace_env;
   pp.max_qtiles = (max_ext + TOK - 1) / TOK;
   const int64_t items = int64_t(pp.max_qtiles) * p.h_kv * (p.cascade ? p.n_kv_splits : batch);
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   const int grid = int(items < sms ? items : sms);   // persistent: one CTA per SM
   if (p.pdl) {
     cudaLaunchConfig_t cfg{};

@@ -11,6 +11,43 @@
 
 namespace rx {
 
+// Every workspace a call takes (include/rx.h "Workspaces") starts with a 256-byte header that
+// holds the persistent extend kernel's work counters ([0] next work index, [1] CTAs finished).
+// It must be zero before the workspace is first used; every call leaves it zero again (the last
+// CTA of an extend grid resets it).  Partial buffers follow the header.  Keeping the counters in
+// the caller's workspace (not in a __device__ global) makes calls on different streams with
+// different workspaces independent.
+constexpr size_t kWsHeader = 256;
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
+// per device context, so a process that drives several GPUs sets it on each.
+template <typename Kern>
+inline cudaError_t ensure_smem_attr(Kern* kern, int bytes) {
+  static unsigned long long done = 0;   // bit d = set on device d
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
+  return e;
+}
+
+// SM count of the current device (cached per device)
+inline int device_sms() {
+  static int sms[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  int& v = sms[dev & 63];
+  if (!v) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    v = n > 0 ? n : 148;
+  }
+  return v;
+}
+
 struct DecodeParams {
   const __nv_bfloat16* q;       // [B, h_q, HD]
   const __nv_bfloat16* kpool;   // [S, h_kv, HD]
@@ -90,6 +127,7 @@ struct ExtendParams {
   // the decode (hence the previous step's merge) before writing partials, and one thread per CTA
   // waits before exiting, so the merge that waits on this grid also sees the decode's partials
   int pdl;
+  int* sched;                   // [2] work counters: the caller's workspace header (kWsHeader)
 };
 
 struct DecodePlan {
@@ -116,7 +154,7 @@ inline size_t decode_ws_bytes(int h_q, int head_dim, int batch, int max_seq_len,
   DecodePlan pl = plan_decode(batch, h_kv, max_seq_len);
   if (pl.max_splits <= 1) return 0;
   const size_t n = size_t(batch) * h_q * pl.max_splits;
-  return n * head_dim * sizeof(float) + n * sizeof(float) + 256;
+  return kWsHeader + n * head_dim * sizeof(float) + n * sizeof(float) + 256;
 }
 
 // Cascade plan (shared-prefix decode): the shared prefix [0, shared_len) is cut
@@ -160,7 +198,7 @@ inline CascadePlan plan_cascade(int batch, int h_kv, int group, int max_seq_len,
 inline size_t cascade_ws_bytes(int h_q, int head_dim, int batch, int h_kv, int max_seq_len, int shared_len) {
   CascadePlan c = plan_cascade(batch, h_kv, h_q / h_kv, max_seq_len, shared_len);
   const size_t n = size_t(batch) * h_q * c.total_splits;
-  return n * head_dim * sizeof(float) + n * sizeof(float) + 256;
+  return kWsHeader + n * head_dim * sizeof(float) + n * sizeof(float) + 256;
 }
 
 cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,

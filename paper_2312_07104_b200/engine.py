@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from rxgen.hashing import prefix_hashes, next_token, splitmix64_int, MASK64
-from rxgen.values import gen_values, KIND_K, KIND_V, KIND_Q
+from rxgen.values import gen_values, gen_values_np, KIND_K, KIND_V, KIND_Q
 
 from . import api
 
@@ -98,10 +98,29 @@ class CallPlan:
 class InputBank:
     """q / k / v of every attention call of a workload, on the device, packed per call."""
 
-    def __init__(self, calls, shape, heads_q, heads_kv, device, q_scale=1.0):
+    def __init__(self, calls, shape, heads_q, heads_kv, device, q_scale=1.0, host=False):
+        """host=True: values are generated on the host (rxgen.gen_values_np) into one pinned buffer
+        and moved with ONE host-to-device copy (no generator kernels on the device: smoke() uses this
+        so a launch list of the run shows only the rx kernels)."""
         self.ext = []
         self.dec = []
         hd = shape.head_dim
+        if host:
+            parts = []
+            for c in calls:
+                h = np.asarray(c.hashes, dtype=np.uint64)
+                parts.append([gen_values_np(h, heads_q, KIND_Q, hd, scale=q_scale),
+                              gen_values_np(h, heads_kv, KIND_K, hd), gen_values_np(h, heads_kv, KIND_V, hd)])
+            flat = np.concatenate([a.ravel() for tr in parts for a in tr]) if parts else np.zeros(0, np.float32)
+            buf = torch.from_numpy(flat).to(torch.bfloat16).pin_memory().to(device, non_blocking=False)
+            off = 0
+            for c, tr in zip(calls, parts):
+                views = []
+                for a in tr:
+                    views.append(buf[off:off + a.size].view(a.shape))
+                    off += a.size
+                (self.ext if c.kind == "extend" else self.dec).append(tuple(views))
+            return
         for c in calls:
             h = c.hashes
             q = gen_values(h, heads_q, KIND_Q, hd, scale=q_scale, device=device)
@@ -520,7 +539,7 @@ class Engine:
             self._rtt = dstage[hdr:].view(R, stride)
         ws_n = api.rx_decode_workspace_bytes(self.cfg, R, stride)
         if self._ws is None or self._ws.numel() < ws_n:
-            self._ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=dev)
+            self._ws = torch.zeros(max(ws_n, 1), dtype=torch.uint8, device=dev)
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         chunks = self._gather_chunks(ext) if (self.gather is not None and hasattr(self.gather, "start")) else None
         ev0 = self._tbeg()
@@ -532,7 +551,7 @@ class Engine:
             # every row shares cached positions [0, shared): attend them once for all rows (cascade)
             ws_n = api.rx_extend_cascade_workspace_bytes(self.cfg, total, shared)
             if self._ws.numel() < ws_n:
-                self._ws = torch.empty(2 * ws_n, dtype=torch.uint8, device=dev)
+                self._ws = torch.zeros(2 * ws_n, dtype=torch.uint8, device=dev)
             api.rx_extend_cascade(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
                                   dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3], total,
                                   int(ext.max()), int(prefix.max()), shared, q, k_new, v_new, self.k_pool,
@@ -626,7 +645,7 @@ class Engine:
         d_all = stage.to(dev, non_blocking=True)
         self._pinned_done(name)
         if need > self._ws.numel():
-            self._ws = torch.empty(2 * need, dtype=torch.uint8, device=dev)   # geometric growth
+            self._ws = torch.zeros(2 * need, dtype=torch.uint8, device=dev)   # geometric growth
         # timing: one event pair around the whole run of back-to-back decode calls (per-call events
         # on ~2000 calls per C3 step would perturb the step); per call when outputs are gathered
         # (TP), so the all-gather stays outside the kernel brackets
@@ -787,9 +806,9 @@ class Engine:
         return self
 
 
-def plan_and_bank(wl, device="cuda", tp_rank=0, tp_size=1, q_scale=1.0, policy="lspf"):
+def plan_and_bank(wl, device="cuda", tp_rank=0, tp_size=1, q_scale=1.0, policy="lspf", host_gen=False):
     """Plan pass + input generation (untimed setup).  Returns (plan engine, InputBank)."""
     plan = Engine(wl, device=device, tp_rank=tp_rank, tp_size=tp_size, plan_only=True, policy=policy)
     plan.run_workload()
-    bank = InputBank(plan.calls, wl.shape, plan.heads_q, plan.heads_kv, device, q_scale=q_scale)
+    bank = InputBank(plan.calls, wl.shape, plan.heads_q, plan.heads_kv, device, q_scale=q_scale, host=host_gen)
     return plan, bank

@@ -69,7 +69,7 @@ def main():
         vn = torch.randn_like(kn)
         o = torch.empty_like(q)
         lens = torch.full((B,), L, dtype=torch.int32, device=dev)
-        ws = torch.empty(max(rx.rx_decode_cascade_workspace_bytes(cfg, B, L, P),
+        ws = torch.zeros(max(rx.rx_decode_cascade_workspace_bytes(cfg, B, L, P),
                              rx.rx_decode_workspace_bytes(cfg, B, L)) + 1, dtype=torch.uint8, device=dev)
         ms_c = timeit(lambda: rx.rx_decode_cascade_append(cfg, rtt, None, lens, L, P, q, kn, vn, new, kp, vp, o, ws))
         ms_p = timeit(lambda: rx.rx_decode_append(cfg, rtt, None, lens, L, q, kn, vn, new, kp, vp, o, ws))
@@ -93,7 +93,7 @@ def main():
         q = torch.randn((B, h_q, hd), device=dev, generator=g).to(torch.bfloat16)
         o = torch.empty_like(q)
         lens = torch.full((B,), L, dtype=torch.int32, device=dev)
-        ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, L) + 1, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(rx.rx_decode_workspace_bytes(cfg, B, L) + 1, dtype=torch.uint8, device=dev)
         ms = timeit(lambda: rx.rx_decode(cfg, rtt, None, lens, L, q, kp, vp, o, ws))
         uniq = (L if a.shared_prefix else B * L)
         byt = uniq * h_kv * hd * 4 + 2 * B * h_q * hd * 2 + 4 * B * L

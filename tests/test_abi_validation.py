@@ -40,7 +40,8 @@ def test_empty_calls_are_ok_and_null_buffers_invalid():
 
 def test_workspace_queries():
     c = cfg()
-    assert lib.rx_extend_workspace_bytes(C.byref(c), 4, 100) == 0
+    assert lib.rx_extend_workspace_bytes(C.byref(c), 4, 100) == 256      # the work-counter header (rx.h)
+    assert lib.rx_extend_workspace_bytes(C.byref(c), 0, 100) == 0
     small = lib.rx_decode_workspace_bytes(C.byref(c), 256, 512)
     big = lib.rx_decode_workspace_bytes(C.byref(c), 4, 65536)
     assert small == 0 and big > 0                       # one split needs no workspace; splits do

@@ -46,17 +46,15 @@ def test_dp_evictions_reach_router():
     wl = workloads.c1(num_slots=300)
     from rxgen.workloads import Request
     W = 2
-    cl = DPCluster(wl, W, plan_only=True, load_weight=1.0)
+    cl = DPCluster(wl, W, plan_only=True, load_weight=1.0, record=True)
     for b in range(6):
         pre = rng.integers(1, 30000, 60).astype(np.int32)
         batch = [Request(np.concatenate([pre, rng.integers(1, 30000, 20).astype(np.int32)]), 3, f"b{b}r{i}")
                  for i in range(4)]
         cl.run_batch(batch)
     assert cl.router.rx_router_queue_len() == 0
-    for e_i, e in enumerate(cl.workers):
-        assert any(t[0] == "evict" for t in e.trace) or True
+    assert any(t[0] == "evict" for e in cl.workers for t in e.trace)     # the pools did evict
     # every router claim is backed by the worker's tree
-    probe = [r for r in []]
     for w, e in enumerate(cl.workers):
         dump = e.cache.rx_dump_json()
         stack = [(dump, [])]

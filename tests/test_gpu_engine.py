@@ -148,6 +148,31 @@ def test_c3_full_size_sampled():
     assert sum(1 for k in oe.outputs if k[0] == "decode") >= 12
 
 
+def test_c2_full_size_sampled():
+    """BASELINE C2 at full size (Llama-2-7B 32/32/128, 5-shot prefix of 1536 tokens, batch 64, new
+    U[64,192], 64 decode steps — cascade decode over the shared prefix): tree trace bit-exact over the
+    whole run; every row of the hint extend at tile boundaries, first/middle/last rows of 6 requests of
+    the batch extend, and 4 requests at decode steps 0, 31 and 63 within tolerance."""
+    wl = workloads.c2()
+
+    def re(call, seqs):
+        if call == 0:
+            return [(0, j) for j in (0, 1, 127, 128, 767, 1534)]
+        out = []
+        for i in (0, 1, 17, 31, 50, 63):
+            n = seqs[i].n_prompt - seqs[i].prefix_len
+            out += [(i, j) for j in sorted({0, n // 2, n - 1})]
+        return out
+
+    def rd(call, step, running):
+        return [0, 21, 42, 63] if step in (0, 31, 63) else []
+
+    e = _run_gpu(wl)
+    oe = _compare(e, wl, re, rd)
+    assert oe.trace == e.trace
+    assert sum(1 for k in oe.outputs if k[0] == "decode") == 12
+
+
 def test_c4_tot_full_parity():
     """C4 at full size: tree-of-thought under Alg. 1 admission with the pool at
     60% of the tree's distinct tokens (evictions between waves)."""
@@ -230,3 +255,15 @@ def test_duplicate_slots_freed_and_reused_mid_phase():
     oe = _compare(e, wl, _all_ext, _all_dec)
     assert oe.trace == e.trace
     assert any(t[0] == "insert" and t[3] > 0 for t in e.trace)      # duplicates were freed
+
+
+def test_host_generated_bank_bitwise_equal():
+    """InputBank(host=True) (numpy generator + one H2D, used by smoke()) holds exactly the device
+    generator's bits."""
+    from paper_2312_07104_b200.engine import InputBank
+    wl = workloads.c1()
+    plan, bank = plan_and_bank(wl, "cuda")
+    hb = InputBank(plan.calls, wl.shape, plan.heads_q, plan.heads_kv, "cuda", host=True)
+    for a, b in zip(bank.ext + bank.dec, hb.ext + hb.dec):
+        for x, y in zip(a, b):
+            assert x.shape == y.shape and torch.equal(x, y)

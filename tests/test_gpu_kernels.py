@@ -97,7 +97,7 @@ def test_decode_vs_oracle(h_q, h_kv, hd, lens, q_scale):
     kp, vp = kall.cuda(), vall.cuda()
     o = torch.empty((B, h_q, hd), dtype=torch.bfloat16, device="cuda")
     ws_n = rx.rx_decode_workspace_bytes(cfg, B, max(lens))
-    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(ws_n, 1), dtype=torch.uint8, device="cuda")
     rx.rx_decode(cfg, torch.from_numpy(rtt).cuda(), None, torch.tensor(lens, dtype=torch.int32, device="cuda"),
                  max(lens), q.cuda(), kp, vp, o, ws)
     torch.cuda.synchronize()
@@ -126,7 +126,7 @@ def test_decode_rows_indirection():
     cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
     o1 = torch.empty((3, h_q, hd), dtype=torch.bfloat16, device="cuda")
     o2 = torch.empty_like(o1)
-    ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, 3, 300) + 1, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(rx.rx_decode_workspace_bytes(cfg, 3, 300) + 1, dtype=torch.uint8, device="cuda")
     rx.rx_decode(cfg, rtt, None, torch.tensor(lens, dtype=torch.int32, device="cuda"), 257, q, kp, vp, o1, ws)
     perm = [2, 0, 1]
     rx.rx_decode(cfg, rtt, torch.tensor(perm, dtype=torch.int32, device="cuda"),
@@ -229,7 +229,7 @@ def test_extend_decode_consistency():
     q = _vals(rng, B, h_q, KIND_Q, hd).cuda()
     cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
     od = torch.empty((B, h_q, hd), dtype=torch.bfloat16, device="cuda")
-    ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, 800) + 1, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(rx.rx_decode_workspace_bytes(cfg, B, 800) + 1, dtype=torch.uint8, device="cuda")
     rx.rx_decode(cfg, rtt_d, None, torch.tensor(lens, dtype=torch.int32, device="cuda"), 700, q, kpool, vpool, od, ws)
     last = torch.from_numpy(np.array([rtt[b, L - 1] for b, L in enumerate(lens)], dtype=np.int64)).cuda()
     oe = torch.empty_like(od)
@@ -339,7 +339,7 @@ def test_cascade_decode_vs_oracle(h_q, h_kv, hd, B, shared, contig, q_scale):
     cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
     seq = torch.tensor(lens, dtype=torch.int32, device="cuda")
     new_d = torch.from_numpy(new).cuda()
-    ws = torch.empty(rx.rx_decode_cascade_workspace_bytes(cfg, B, max(lens), shared) + 1, dtype=torch.uint8,
+    ws = torch.zeros(rx.rx_decode_cascade_workspace_bytes(cfg, B, max(lens), shared) + 1, dtype=torch.uint8,
                      device="cuda")
     kp, vp, rtt_d = kpool.cuda(), vpool.cuda(), torch.from_numpy(rtt).cuda()
     o = torch.full((B, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
@@ -347,7 +347,7 @@ def test_cascade_decode_vs_oracle(h_q, h_kv, hd, B, shared, contig, q_scale):
     # reference path for the append side effects
     kp2, vp2, rtt2 = kpool.cuda(), vpool.cuda(), torch.from_numpy(rtt).cuda()
     o2 = torch.empty_like(o)
-    ws2 = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, max(lens)) + 1, dtype=torch.uint8, device="cuda")
+    ws2 = torch.zeros(rx.rx_decode_workspace_bytes(cfg, B, max(lens)) + 1, dtype=torch.uint8, device="cuda")
     rx.rx_decode_append(cfg, rtt2, None, seq, max(lens), q, kn.cuda(), vn.cuda(), new_d, kp2, vp2, o2, ws2)
     torch.cuda.synchronize()
     assert torch.equal(kp, kp2) and torch.equal(vp, vp2) and torch.equal(rtt_d, rtt2)
@@ -383,7 +383,7 @@ def _decode_append_check(h_q, h_kv, hd, lens):
     vn = _vals(rng, B, h_kv, KIND_V, hd).cuda()
     cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
     seq = torch.tensor(lens, dtype=torch.int32, device="cuda")
-    ws = torch.empty(rx.rx_decode_workspace_bytes(cfg, B, max(lens)) + 1, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(rx.rx_decode_workspace_bytes(cfg, B, max(lens)) + 1, dtype=torch.uint8, device="cuda")
     new_d = torch.from_numpy(new).cuda()
     # path 1: store + decode
     kp1, vp1, rtt1 = kp.clone(), vp.clone(), torch.from_numpy(rtt).cuda()
@@ -437,7 +437,7 @@ def test_extend_cascade_vs_oracle(h_q, h_kv, hd, B, shared, max_pre_own, max_ext
     cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
     kp, vp = kpool.cuda(), vpool.cuda()
     o = torch.full((N, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
-    ws = torch.empty(rx.rx_extend_cascade_workspace_bytes(cfg, N, shared), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(rx.rx_extend_cascade_workspace_bytes(cfg, N, shared), dtype=torch.uint8, device="cuda")
     rows = torch.arange(B, dtype=torch.int32, device="cuda")
     rx.rx_extend_cascade(cfg, torch.from_numpy(rtt).cuda(), rows, torch.tensor(pre, dtype=torch.int32, device="cuda"),
                          torch.tensor(ext, dtype=torch.int32, device="cuda"), torch.from_numpy(indptr).cuda(), N,
@@ -452,3 +452,55 @@ def test_extend_cascade_vs_oracle(h_q, h_kv, hd, B, shared, max_pre_own, max_ext
     for b in range(B):
         s_new = torch.from_numpy(rtt[b, pre[b]:pre[b] + ext[b]].astype(np.int64)).cuda()
         assert torch.equal(kp[s_new], kn[indptr[b]:indptr[b + 1]].cuda())
+
+
+def test_concurrent_extends_on_two_streams():
+    """Reentrancy (include/rx.h "Streams and concurrency"): two rx_extend calls with different
+    workspaces run concurrently on two streams of one device — each persistent grid hands out its
+    own work items from its own workspace header — and both match the oracle; their workspace
+    headers are zero again afterwards.  Repeated so the grids overlap in time."""
+    rng = np.random.default_rng(77)
+    h_q, h_kv, hd = 32, 8, 128
+    cases = []
+    for c in range(2):
+        B = 12
+        pre = [int(x) for x in rng.integers(0, 900, B)]
+        ext = [int(x) for x in rng.integers(100, 400, B)]
+        S = sum(pre) + sum(ext) + 64
+        rtt = np.zeros((B, max(p + e for p, e in zip(pre, ext))), dtype=np.int32)
+        perm = rng.permutation(np.arange(1, S))
+        off = 0
+        for b in range(B):
+            rtt[b, :pre[b] + ext[b]] = perm[off:off + pre[b] + ext[b]]
+            off += pre[b] + ext[b]
+        N = sum(ext)
+        d = dict(pre=pre, ext=ext, rtt=rtt, N=N, S=S,
+                 kpool=_vals(rng, S, h_kv, KIND_K, hd), vpool=_vals(rng, S, h_kv, KIND_V, hd),
+                 q=_vals(rng, N, h_q, KIND_Q, hd), kn=_vals(rng, N, h_kv, KIND_K, hd),
+                 vn=_vals(rng, N, h_kv, KIND_V, hd),
+                 indptr=np.concatenate([[0], np.cumsum(ext)]).astype(np.int32))
+        cases.append(d)
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    dev = []
+    for d in cases:
+        dev.append(dict(rtt=torch.from_numpy(d["rtt"]).cuda(), pre=torch.tensor(d["pre"], dtype=torch.int32).cuda(),
+                        ext=torch.tensor(d["ext"], dtype=torch.int32).cuda(), ind=torch.from_numpy(d["indptr"]).cuda(),
+                        q=d["q"].cuda(), kn=d["kn"].cuda(), vn=d["vn"].cuda(), kp=d["kpool"].cuda(),
+                        vp=d["vpool"].cuda(),
+                        o=torch.full((d["N"], h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda"),
+                        ws=torch.zeros(rx.rx_extend_workspace_bytes(cfg, len(d["pre"]), max(d["ext"])),
+                                       dtype=torch.uint8, device="cuda")))
+    torch.cuda.synchronize()
+    for _ in range(20):
+        for d, x, st in zip(cases, dev, streams):
+            rx.rx_extend(cfg, x["rtt"], None, x["pre"], x["ext"], x["ind"], d["N"], max(d["ext"]), max(d["pre"]),
+                         x["q"], x["kn"], x["vn"], x["kp"], x["vp"], x["o"], x["ws"], stream=st)
+    torch.cuda.synchronize()
+    for d, x in zip(cases, dev):
+        assert int(x["ws"].count_nonzero()) == 0
+        pool = A.OraclePool(d["S"], h_kv, hd)
+        pool.store(np.arange(d["S"]), d["kpool"].float().numpy(), d["vpool"].float().numpy())
+        ref = A.extend(pool, [d["rtt"][b] for b in range(len(d["pre"]))], d["pre"], d["ext"], d["q"].float().numpy(),
+                       d["kn"].float().numpy(), d["vn"].float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
+        _cmp(x["o"], ref, "concurrent extend")

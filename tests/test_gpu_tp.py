@@ -6,8 +6,12 @@ local shapes a P-GPU run uses.
   operations are the same") and equals the 1-GPU trace;
 * the shards' outputs, reassembled in global head order, match the 1-GPU run
   within the attention tolerance (different local shapes may change the
-  split-KV partition, hence summation order, so not bitwise).
+  split-KV partition, hence summation order, so not bitwise);
+* the reassembled outputs match the fp64 ORACLE on every row within the
+  north-star tolerance (max-abs 2e-2, mean-abs 2e-3).
 """
+import types
+
 import numpy as np
 import pytest
 import torch
@@ -49,6 +53,12 @@ def test_fake_tp_matches_single_gpu(make, P):
         err = (o_tp.float() - o_full.float()).abs().max().item()
         worst = max(worst, err)
     assert worst <= 2e-2, worst
+    # the re-assembled TP output against the oracle, every row (tests/test_gpu_engine.py::_compare)
+    from test_gpu_engine import _compare, _all_ext, _all_dec
+    tp = types.SimpleNamespace(outputs=[(kind, torch.cat([s.outputs[ci][1] for s in shards], dim=1), meta)
+                                        for ci, (kind, _, meta) in enumerate(full.outputs)])
+    oe = _compare(tp, wl, _all_ext, _all_dec)
+    assert oe.trace == full.trace
 
 
 def test_chunked_overlapped_gather_world1_nccl():
