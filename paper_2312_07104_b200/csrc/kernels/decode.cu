@@ -27,6 +27,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cstdlib>
 
 #include "params.cuh"
@@ -382,6 +385,19 @@ static bool pdl_enabled() {
   return v != 0;
 }
 int pdl_on() { return pdl_enabled() ? 1 : 0; }
+
+cudaError_t ensure_smem_attr_ptr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;   // (kernel, device) with the attribute set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kern, dev});
+  return e;
+}
 
 template <typename Kern, typename... Args>
 static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {

@@ -20,18 +20,12 @@ namespace rx {
 constexpr size_t kWsHeader = 256;
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
-// per device context, so a process that drives several GPUs sets it on each.
+// per device context, so a process that drives several GPUs sets it on each.  Keyed by the kernel's
+// address (every instantiation of a kernel template has the same function TYPE).
+cudaError_t ensure_smem_attr_ptr(const void* kern, int bytes);   // decode.cu
 template <typename Kern>
 inline cudaError_t ensure_smem_attr(Kern* kern, int bytes) {
-  static unsigned long long done = 0;   // bit d = set on device d
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
-  return e;
+  return ensure_smem_attr_ptr(reinterpret_cast<const void*>(kern), bytes);
 }
 
 // SM count of the current device (cached per device)

@@ -539,7 +539,7 @@ class Engine:
             self._rtt = dstage[hdr:].view(R, stride)
         ws_n = api.rx_decode_workspace_bytes(self.cfg, R, stride)
         if self._ws is None or self._ws.numel() < ws_n:
-            self._ws = torch.zeros(max(ws_n, 1), dtype=torch.uint8, device=dev)
+            self._ws = torch.zeros(max(ws_n, 256), dtype=torch.uint8, device=dev)   # >= the counter header (rx.h)
         o = torch.empty((total, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
         chunks = self._gather_chunks(ext) if (self.gather is not None and hasattr(self.gather, "start")) else None
         ev0 = self._tbeg()
@@ -560,7 +560,7 @@ class Engine:
         elif chunks is None:
             api.rx_extend(self.cfg, self._rtt, dstage[3 * B + 3:4 * B + 3] if rows is not None else None,
                           dstage[0:B], dstage[B + 1:2 * B + 1], dstage[2 * B + 2:3 * B + 3],
-                          total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o)
+                          total, int(ext.max()), int(prefix.max()), q, k_new, v_new, self.k_pool, self.v_pool, o, self._ws)
             nl = api.rx_last_launch_count()
         else:
             # TP: the call runs as request blocks; each block's rows are all-gathered (async, NCCL
@@ -592,7 +592,7 @@ class Engine:
                 d = dchunk[c0:c0 + 4 * n + 1]
                 api.rx_extend(self.cfg, self._rtt, d[3 * n + 1:4 * n + 1], d[0:n], d[n:2 * n], d[2 * n:3 * n + 1],
                               r1 - r0, int(ext[b0:b1].max()), int(prefix[b0:b1].max()), q[r0:r1], k_new[r0:r1],
-                              v_new[r0:r1], self.k_pool, self.v_pool, o[r0:r1])
+                              v_new[r0:r1], self.k_pool, self.v_pool, o[r0:r1], self._ws)
                 nl += api.rx_last_launch_count()
                 handles.append(self.gather.start(o[r0:r1], out, r0, r1))
         self.stats["launches"] += nl + nl0
