@@ -740,15 +740,24 @@ class Engine:
         return float(uniq * row + extra), float(int((pos + 1).sum()) * row + extra)
 
     def timing_summary(self):
-        """{kind: (total ms, launches, calls, total work)} from the recorded events (call after a sync)."""
+        """{kind: [total ms, launches, calls, total work, logical work]} from the recorded events (call
+        after a sync).  work = FLOPs (extend) or algorithmic bytes (decode: distinct pool rows once);
+        logical = the same for extend, every request's rows for decode (paged-equivalent bytes)."""
         out = {}
         for kind, a, b, work, nl, calls in self.timer or []:
             ms = a.elapsed_time(b)
-            t = out.setdefault(kind, [0.0, 0, 0, 0.0])
+            t = out.setdefault(kind, [0.0, 0, 0, 0.0, 0.0])
             t[0] += ms
             t[1] += nl
             t[2] += calls
-            t[3] += sum(self.decode_bytes(w)[0] for w in work) if kind == "decode" else work
+            if kind == "decode":
+                for w in work:
+                    alg, logical = self.decode_bytes(w)
+                    t[3] += alg
+                    t[4] += logical
+            else:
+                t[3] += work
+                t[4] += work
         return out
 
     # ------------------------------------------------------------------ workloads
