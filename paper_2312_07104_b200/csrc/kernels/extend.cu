@@ -8,24 +8,33 @@
 // rows prefix_len.. are this call's k_new/v_new (read directly; rx_extend
 // stores them into their pool slots with a separate launch, A5).
 //
-// B200 design (one CTA per (q tile, kv head, request)):
-//  * M = 128 rows per tile = (128/G tokens) x (G heads of one kv group): GQA
-//    packing makes every K/V tile byte serve G heads (R14);
-//  * warp 0 = TMA producer: Q by a 3-D tiled load; new K/V by 3-D tiled
-//    loads; cached-prefix K/V either by one 3-D tiled load per 64 columns when
-//    the 128 slots of the tile are consecutive (the smallest-first allocator
-//    makes that common for prompt tokens), or by per-lane 16-byte cp.async
-//    gathers into the swizzled layout otherwise (decode-time slots interleave
-//    requests); separate K (3-deep) and V (2-deep) rings with full/empty
-//    mbarriers;
-//  * warp 1 = single-thread UMMA issuer: S = Q K^T (bf16 -> fp32 TMEM,
-//    double-buffered) then O += P V with P read from TMEM (A operand in
-//    tensor memory), all 128x128 / 128xHD tiles, cta_group::1;
-//  * warps 4-7 = softmax: thread = TMEM lane = row; tcgen05.ld the S row,
-//    causal/length mask, online softmax in the log2 domain with lazy O
-//    rescaling (only when the running max grows by > 8), P packed to bf16 and
-//    tcgen05.st over the S columns; epilogue O / l -> bf16 -> global;
-//  * warp 2: TMEM allocation; warp 3: V producer (K and V rings are separate).
+// B200 design — persistent, one CTA (12 warps) per SM, work items handed out
+// dynamically; an item is (PAIR of q tiles A, B; kv head g; request b):
+//  * M = 128 rows per q tile = (128/G tokens) x (G heads of one kv group): GQA
+//    packing makes every K/V tile byte serve G heads (R14).  Tiles A and B are
+//    consecutive token ranges of the same (b, g), so every K/V tile staged in
+//    shared memory feeds two 128-row MMAs (half the L2 -> SMEM traffic per
+//    FLOP of a one-tile CTA);
+//  * TMEM (512 columns) = S_A | S_B | O_A | O_B: two score tiles and two
+//    output accumulators, all fp32;
+//  * two softmax warpgroups (warps 4-7: tile A, warps 8-11: tile B; thread =
+//    TMEM lane = row) ping-pong on the tensor core: the MMA warp issues, per
+//    K/V tile j, O_A += P_A(j-1) V(j-1), S_A(j) = Q_A K(j)^T, then the same for
+//    B, so the tensor core computes one tile's GEMMs while the other tile's
+//    warpgroup runs its softmax.  Issue order makes the TMEM reuse safe (the
+//    MMA pipe executes in order) and makes S_x(j) complete only after
+//    O_x += P_x(j-1) V(j-1), so the softmax may rescale O_x in TMEM as soon as
+//    it sees S_x(j) (lazy rescale: only when a row max grows by > 8 in log2);
+//  * warp 0 = item scheduler + K producer (it takes the next work index just
+//    before the CTA needs it and publishes a descriptor ring in shared memory),
+//    warp 3 = Q + V producer: cached-prefix K/V by one
+//    3-D TMA box per 64 columns when the tile's 128 slots are consecutive (the
+//    smallest-first allocator makes that common for prompt tokens), else
+//    16-byte cp.async gathers written straight into the 128B-swizzled layout;
+//    new K/V by 3-D TMA boxes; K 2-deep and V 3-deep rings (hd 128);
+//  * warp 1 = single-thread tcgen05.mma issuer; warp 2 = TMEM owner;
+//  * setmaxnreg moves registers from the producer warpgroup (64 each) to the
+//    softmax warpgroups (216 each: a whole 128-column S row lives in registers);
 //  * A5 (store new K/V into their slots) is a separate, fully parallel kernel
 //    launched just before on the same stream (store.cu).
 #include <cuda.h>
@@ -49,60 +58,50 @@ struct ExtendMaps {
   CUtensorMap vpool;
 };
 
-constexpr int kExtThreads = 256;
-
+constexpr int kExtThreads = 384;    // 12 warps: 4 producer/MMA/scheduler + 2 softmax warpgroups
+constexpr int kProducerRegs = 64;   // setmaxnreg budget of warps 0-3
+constexpr int kSoftmaxRegs = 216;   // ... and of warps 4-11 (64*128 + 216*256 <= 168*384)
 constexpr int kBN = 128;            // kv tokens per tile
 constexpr int kTileRowBytes = 128;  // 64 bf16 per swizzled row
-#ifndef RX_FENCE
-#define RX_FENCE 1
-#endif
-
-// Development timeline tracer (off unless RX_EXT_TRACE is set at launch): CTA 0
-// stores clock64 per (event code, item/tile index); read back with rx_debug_ext_trace().
-__device__ unsigned long long rx_ext_trace[16 * 1024];   // [code][item & 1023]: clock64, CTA 0 only
-__device__ __forceinline__ void ext_trace(int on, int code, int item) {
-  if (on && blockIdx.x == 0) rx_ext_trace[code * 1024 + (item & 1023)] = clock64();   // plain store, no wait
-}
 
 template <int HD>
 struct ExtCfg {
-  static constexpr int NCB = HD / 64;                         // 64-column blocks
-  static constexpr int Q_BYTES = NCB * 128 * kTileRowBytes;   // one Q tile (double-buffered)
-  static constexpr int KV_BYTES = NCB * kBN * kTileRowBytes;  // one K (or V) tile
-  // K and V live in separate rings: K_j is released as soon as S_j = Q K_j^T
-  // retires, V_j only after P_j V_j, so K can run further ahead (its load
-  // latency is on the critical path of the next softmax).
-  static constexpr int KS = HD == 128 ? 3 : 4;
-  static constexpr int VS = HD == 128 ? 2 : 3;
-  static constexpr int SMEM_DATA = 2 * Q_BYTES + (KS + VS) * KV_BYTES;
+  static constexpr int NCB = HD / 64;                          // 64-column blocks
+  static constexpr int TILE_BYTES = NCB * 128 * kTileRowBytes;  // one 128-row tile (Q, K or V)
+  // K_j is released as soon as both S = Q K_j^T retire, V_j only after both P V_j; V(j) is
+  // fetched when PV(j - VS) retires and needed at PV(j), so gathered (cp.async) V tiles need the
+  // deeper ring: KS 2 / VS 3 measured 787 vs 738 TFLOP/s (KS 3 / VS 2) on half-fragmented C3
+  // histories, and 996 vs 955 on contiguous ones (hd 128).
+  static constexpr int KS = HD == 128 ? 2 : 4;
+  static constexpr int VS = HD == 128 ? 3 : 3;
+  static constexpr int SMEM_DATA = (2 + KS + VS) * TILE_BYTES;  // Q_A, Q_B, K ring, V ring
   static constexpr int SMEM = SMEM_DATA + 1024 /*align*/ + 1024 /*barriers + item ring*/;
-  static constexpr uint32_t TMEM_COLS = 512;                  // S0 | S1 | O0 | O1
-  static constexpr uint32_t O_COL = 256;                      // O buffer b at O_COL + b*HD
+  static constexpr uint32_t TMEM_COLS = 512;                    // S_A | S_B | O_A | O_B
+  static constexpr uint32_t O_COL = 256;                        // O_x at O_COL + x*HD
 };
+static_assert(ExtCfg<128>::SMEM <= 232448, "extend kernel exceeds the 227 KB opt-in shared memory");
 
-// One work item = (q tile t, kv head g, request b), dealt to the persistent
-// CTAs round-robin; every role of a CTA walks the same list.
+// One work item = (q tiles t0 and t0+1, kv head g, request b); every role of a CTA walks the
+// same list.  n[x] = K/V tiles q tile x attends to (0: tile x is past the request's rows).
 struct ExtItem {
-  int b, g, t, P, ext, qo, n_pre, n_tiles;
+  int b, g, t0, P, ext, qo, n_pre;
+  int n[2];
   int tile0;            // first prefix tile (cascade chunk), 0 otherwise
   int split;            // cascade chunk index
   const int32_t* slots;
 };
 
-// Item ring: warp 2 resolves the CTA's work items (32 candidates per round, one
-// per lane, so the request-array loads overlap) and publishes descriptors in
-// shared memory; the 7 consumers (K producer, MMA, V producer, 4 softmax warps)
-// read them instead of each walking the list with dependent global loads.
-constexpr int kRing = 8;
-constexpr int kRingConsumers = 7;
+// Item ring: warp 0 resolves the CTA's work items and publishes descriptors in shared memory;
+// the 10 consumer warps (MMA, Q/V producer, 8 softmax) read them.
+constexpr int kRing = 2;
+constexpr int kRingConsumers = 10;
 
 struct RingCursor {
   int slot = 0;
   uint32_t phase = 0;
 };
 
-// all lanes of the calling warp (or the lone MMA lane) read the descriptor;
-// `arrive` marks the lane that releases the slot
+// all lanes of the calling warp read the descriptor; `arrive` marks the lane that releases it
 __device__ __forceinline__ bool ring_pop(ExtItem& I, RingCursor& c, const ExtItem* ring, uint64_t* full,
                                          uint64_t* empty, bool arrive) {
   mbar_wait(full + c.slot, c.phase);
@@ -116,20 +115,21 @@ __device__ __forceinline__ bool ring_pop(ExtItem& I, RingCursor& c, const ExtIte
 }
 
 template <int TOK>
-__device__ __forceinline__ bool ext_item(const ExtendParams& p, int qt, int w, ExtItem& it) {
-  // (request, kv head) outer, q tile inner (heaviest first): the q tiles of
-  // one (b, g) run on neighbouring CTAs at the same time, so that head's
-  // cached prefix is read from HBM once and re-served from L2.
+__device__ __forceinline__ bool ext_item(const ExtendParams& p, int qp, int w, ExtItem& it) {
+  // (request, kv head) outer, q-tile pair inner (heaviest first): the pairs of one (b, g) run
+  // on neighbouring CTAs at the same time, so that head's cached prefix is read from HBM once
+  // and re-served from L2.
+  const int pair = qp - 1 - w % qp;
+  it.t0 = 2 * pair;
   if (p.cascade) {
-    // (kv head, prefix chunk) outer, q tile inner: all q tiles of one chunk
-    // share its K/V through L2.  One virtual request (b = 0) of `batch` rows.
-    const int gs = w / qt;
-    it.t = qt - 1 - w % qt;
+    // (kv head, prefix chunk) outer: all q tiles of one chunk share its K/V through L2.
+    // One virtual request (b = 0) of `batch` rows; no mask except the prefix end.
+    const int gs = w / qp;
     it.g = gs % p.h_kv;
     it.split = gs / p.h_kv;
     it.b = 0;
     it.ext = p.batch;
-    if (it.t * TOK >= it.ext) return false;
+    if (it.t0 * TOK >= it.ext) return false;
     it.P = p.cas_prefix;
     it.qo = 0;
     const int row = p.rows ? p.rows[0] : 0;
@@ -137,25 +137,128 @@ __device__ __forceinline__ bool ext_item(const ExtendParams& p, int qt, int w, E
     const int total = (it.P + kBN - 1) / kBN;
     it.tile0 = it.split * p.kv_split_tiles;
     it.n_pre = min(p.kv_split_tiles, total - it.tile0);
-    it.n_tiles = it.n_pre;
+    it.n[0] = it.n_pre;
+    it.n[1] = (it.t0 + 1) * TOK < it.ext ? it.n_pre : 0;
     return it.n_pre > 0;
   }
   it.tile0 = 0;
   it.split = 0;
-  const int bg = w / qt;
-  it.t = qt - 1 - w % qt;
+  const int bg = w / qp;
   it.g = bg % p.h_kv;
   it.b = bg / p.h_kv;
   it.ext = p.extend_lens[it.b];
-  if (it.t * TOK >= it.ext) return false;
+  if (it.t0 * TOK >= it.ext) return false;
   it.P = p.prefix_lens[it.b];
   it.qo = p.qo_indptr[it.b];
   const int row = p.rows ? p.rows[it.b] : it.b;
   it.slots = p.rtt + int64_t(row) * p.rtt_stride;
-  const int rel_end = min(it.ext, (it.t + 1) * TOK);
   it.n_pre = (it.P + kBN - 1) / kBN;
-  it.n_tiles = it.n_pre + (rel_end + kBN - 1) / kBN;
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int t = it.t0 + x;
+    const int rel_end = min(it.ext, (t + 1) * TOK);
+    it.n[x] = t * TOK < it.ext ? it.n_pre + (rel_end + kBN - 1) / kBN : 0;
+  }
   return true;
+}
+
+// Where the rows of K/V tile j of item I come from, resolved BEFORE the producer waits for a free
+// ring stage (the slot-index loads then overlap that wait): a prefix tile whose 128 slots are
+// consecutive is one 3-D TMA box per 64 columns (`tma`, starting at slot s0); a fragmented prefix
+// tile is gathered row by row (slot_r[i] = slot of row lane + 32 i, -1 past the prefix); a
+// new-KV tile is a TMA box of k_new / v_new.
+struct TileSrc {
+  bool tma;
+  int s0;
+  int slot_r[4];
+};
+
+__device__ __forceinline__ TileSrc probe_kv_tile(const ExtItem& I, int j, int lane) {
+  TileSrc t;
+  t.tma = true;
+  t.s0 = 0;
+  if (j < I.n_pre) {
+    const int jt = I.tile0 + j;                   // absolute prefix tile (cascade chunks)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int pos = jt * kBN + lane + 32 * i;
+      t.slot_r[i] = pos < I.P ? I.slots[pos] : -1;
+    }
+    t.s0 = __shfl_sync(0xffffffffu, t.slot_r[0], 0);   // (jt*kBN < P: the tile has >= 1 cached row)
+    bool contig = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) contig &= t.slot_r[i] == t.s0 + lane + 32 * i;
+    t.tma = __all_sync(0xffffffffu, contig);
+  }
+  return t;
+}
+
+// One K or V tile j of item I into ring stage at smem address d (warp-collective; lane 0 issues
+// TMA).  Gathers are per-lane 16-byte cp.async written straight into the 128B-swizzled layout
+// (chunk k of row r -> chunk k ^ (r & 7)), rows past the prefix zero-filled.  Every lane arrives
+// on `full` (TMA: lane 0 with expect_tx, others plainly; cp.async: .noinc arrivals).
+template <int HD>
+__device__ __forceinline__ void load_kv_tile(const ExtItem& I, int j, const TileSrc& t, uint32_t d, uint64_t* full,
+                                             const CUtensorMap* m_pool, const CUtensorMap* m_new,
+                                             const __nv_bfloat16* base_g, int h_kv, int lane) {
+  using C = ExtCfg<HD>;
+  if (t.tma) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(full, C::TILE_BYTES);
+      if (j < I.n_pre) {
+#pragma unroll
+        for (int c = 0; c < C::NCB; ++c) tma_load_3d(d + c * kBN * kTileRowBytes, m_pool, full, c * 64, I.g, t.s0);
+      } else {
+        const int nn = j - I.n_pre;
+#pragma unroll
+        for (int c = 0; c < C::NCB; ++c)
+          tma_load_3d(d + c * kBN * kTileRowBytes, m_new, full, c * 64, I.g, I.qo + nn * kBN);
+      }
+    } else {
+      mbar_arrive(full);
+    }
+  } else {
+    constexpr int CPR = HD / 8, RPI = 32 / CPR;
+    const int ch = lane % CPR, rsub = lane / CPR;
+    const uint32_t dcol = d + (ch >> 3) * kBN * kTileRowBytes;
+#pragma unroll
+    for (int rr = 0; rr < kBN; rr += RPI) {
+      const int row = rr + rsub;
+      const int sl = __shfl_sync(0xffffffffu, t.slot_r[rr / 32], row & 31);
+      const bool ok = sl > 0;
+      const __nv_bfloat16* src = base_g + (int64_t(ok ? sl : 0) * h_kv + I.g) * HD + ch * 8;
+      cp_async_16(dcol + row * kTileRowBytes + (((ch & 7) ^ (row & 7)) << 4), src, ok ? 16u : 0u);
+    }
+    cp_async_mbar_arrive_noinc(full);
+  }
+}
+
+// exp2 of one half (64 columns) of a score row, its row-sum contribution (two packed fp32-pair
+// accumulators), and P (bf16 pairs) into the first 32 TMEM columns of that half's S columns.
+// Packed FFMA2 / FADD2 do the scale-subtract, the sums and the polynomial two columns per issue
+// slot (the softmax warps are issue-bound).  MUFU ex2 is the other limiter (16/clk/SM vs 8192 MMA
+// FLOP/clk): with POLY (an unmasked tile) every 4th column pair is evaluated on the FMA pipe
+// instead (exp2_poly3; masked tiles need exact zeros, so MUFU only).
+template <bool POLY>
+__device__ __forceinline__ void softmax_half(const float* sv, int half, float sc, float nm, uint64_t* rs,
+                                             uint32_t t_s) {
+  uint32_t pk[kBN / 4];
+  const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(nm, nm);
+#pragma unroll
+  for (int c = 0; c < kBN / 4; ++c) {
+    const int col = half * (kBN / 2) + 2 * c;
+    float x0, x1, e0, e1;
+    f2_unpack(f2_fma(f2_pack(sv[col], sv[col + 1]), sc2, nm2), x0, x1);
+    if (POLY && (c & 3) == 3) {
+      exp2_poly3_x2(x0, x1, e0, e1);
+    } else {
+      e0 = fast_exp2(x0);
+      e1 = fast_exp2(x1);
+    }
+    rs[c & 1] = f2_add(rs[c & 1], f2_pack(e0, e1));
+    pk[c] = pack_bf16(e0, e1);
+  }
+  tmem_st32(t_s + half * 32, pk);
 }
 
 template <int HD, int G>
@@ -165,28 +268,26 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   constexpr int TOK = 128 / G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sq = smem_u32(smem);                 // Q buffer qb at sq + qb*Q_BYTES
-  const uint32_t sk = sq + 2 * C::Q_BYTES;            // K stage s at sk + s*KV_BYTES
-  const uint32_t sv_ = sk + C::KS * C::KV_BYTES;      // V stage s at sv_ + s*KV_BYTES
+  const uint32_t sq = smem_u32(smem);                 // Q tile x at sq + x*TILE_BYTES
+  const uint32_t sk = sq + 2 * C::TILE_BYTES;         // K stage s at sk + s*TILE_BYTES
+  const uint32_t sv_ = sk + C::KS * C::TILE_BYTES;    // V stage s at sv_ + s*TILE_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA);
-  uint64_t* q_full = bars;                            // [2]
+  uint64_t* q_full = bars;                            // [2] per q tile x
   uint64_t* q_empty = bars + 2;                       // [2]
   uint64_t* k_full = bars + 4;                        // [KS]
   uint64_t* k_empty = k_full + C::KS;                 // [KS]
   uint64_t* v_full = k_empty + C::KS;                 // [VS]
   uint64_t* v_empty = v_full + C::VS;                 // [VS]
-  uint64_t* s_full = v_empty + C::VS;                 // [2]
-  uint64_t* p_full = s_full + 2;                      // [2]
-  uint64_t* o_done = p_full + 2;                      // one phase per P.V
-  uint64_t* o_ready = o_done + 1;                     // [2] one phase per item (its last P.V)
-  uint64_t* o_free = o_ready + 2;                     // [2] epilogue has read O[b]
-  uint64_t* desc_full = o_free + 2;                   // [kRing] item descriptors published
-  uint64_t* desc_empty = desc_full + kRing;           // [kRing] ... and consumed by all 7 roles
+  uint64_t* s_full = v_empty + C::VS;                 // [2] S_x(j) landed (one phase per tile of x)
+  uint64_t* p_full = s_full + 2;                      // [2] P_x(j) written (128 arrivals)
+  uint64_t* o_ready = p_full + 2;                     // [2] O_x final (one phase per item of x)
+  uint64_t* desc_full = o_ready + 2;                  // [kRing] item descriptors published
+  uint64_t* desc_empty = desc_full + kRing;           // [kRing] ... and consumed by the 10 other warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(desc_empty + kRing);
   ExtItem* ring = reinterpret_cast<ExtItem*>(smem + C::SMEM_DATA + 512);
 
-  const int qt = p.max_qtiles;
-  const int W = p.cascade ? qt * p.h_kv * p.n_kv_splits : qt * p.h_kv * p.batch;
+  const int qp = (p.max_qtiles + 1) / 2;              // q-tile pairs per (b, g)
+  const int W = p.cascade ? qp * p.h_kv * p.n_kv_splits : qp * p.h_kv * p.batch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -196,7 +297,6 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
       mbar_init(o_ready + i, 1);
-      mbar_init(o_free + i, 128);
     }
     for (int s = 0; s < C::KS; ++s) {
       mbar_init(k_full + s, 32);   // all producer lanes arrive (TMA: 1 expect_tx + 31; cp.async: 32 noinc)
@@ -206,7 +306,6 @@ __global__ void __launch_bounds__(kExtThreads, 1)
       mbar_init(v_full + s, 32);
       mbar_init(v_empty + s, 1);
     }
-    mbar_init(o_done, 1);
     for (int i = 0; i < kRing; ++i) {
       mbar_init(desc_full + i, 1);
       mbar_init(desc_empty + i, kRingConsumers);
@@ -219,187 +318,202 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 3) {
-    // ------------------------------------------------------------ producers: warp 0 = Q + K, warp 3 = V
-    const bool is_v = warp == 3;
-    const int NS = is_v ? C::VS : C::KS;
-    uint64_t* full = is_v ? v_full : k_full;
-    uint64_t* empty = is_v ? v_empty : k_empty;
-    const uint32_t base_s = is_v ? sv_ : sk;
-    const CUtensorMap* m_pool = is_v ? &maps.vpool : &maps.kpool;
-    const __nv_bfloat16* base_g = is_v ? p.vpool : p.kpool;
-    const CUtensorMap* m_new = is_v ? &maps.vnew : &maps.knew;
+  if (warp == 0) {
+    // ------------------------------------------------------------ item scheduler + K producer
+    // Items are handed out dynamically from the work counter in the caller's workspace, so ragged
+    // batches (items of 1..N tiles, some q tiles absent) balance across SMs.  This warp takes the
+    // next work index only once it has issued every K load of its current item, i.e. just before
+    // the CTA needs it: consecutive indices (the q-tile pairs of one (b, g)) then start within a
+    // short window on different SMs and share that head's cached prefix through L2 (fetching
+    // further ahead spreads their start times over an item's duration, and the prefix is evicted
+    // between them: measured 2x the DRAM bytes on fragmented C3 histories).  Descriptors go to
+    // the other warps through the ring.
+    regs_dealloc<kProducerRegs>();
     if (lane == 0) {
-      if (!is_v) tma_prefetch_desc(&maps.q);
-      tma_prefetch_desc(m_new);
-      tma_prefetch_desc(m_pool);
+      tma_prefetch_desc(&maps.knew);
+      tma_prefetch_desc(&maps.kpool);
     }
-    int it = 0, jg = 0;
+    RingCursor c;
+    auto publish = [&](const ExtItem& it) {
+      mbar_wait(desc_empty + c.slot, c.phase ^ 1);
+      if (lane == 0) {
+        ring[c.slot] = it;
+        mbar_arrive(desc_full + c.slot);
+      }
+      __syncwarp();
+      if (++c.slot == kRing) {
+        c.slot = 0;
+        c.phase ^= 1;
+      }
+    };
+    auto next = [&](ExtItem& it) -> bool {
+      for (;;) {
+        int w = 0;
+        if (lane == 0) w = atomicAdd(&p.sched[0], 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= W) return false;
+        if (ext_item<TOK>(p, qp, w, it)) return true;
+      }
+    };
+    int jg = 0;
+    ExtItem I;
+    bool have = next(I);
+    while (have) {
+      publish(I);
+      const int N = max(I.n[0], I.n[1]);
+      for (int j = 0; j < N; ++j, ++jg) {
+        const int st = jg % C::KS, rnd = jg / C::KS;
+        const TileSrc t = probe_kv_tile(I, j, lane);
+        mbar_wait(k_empty + st, (rnd & 1) ^ 1);
+        load_kv_tile<HD>(I, j, t, sk + st * C::TILE_BYTES, k_full + st, &maps.kpool, &maps.knew, p.kpool, p.h_kv,
+                         lane);
+      }
+      have = next(I);
+    }
+    ExtItem stop{};
+    stop.b = -1;
+    publish(stop);
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ Q + V producer
+    regs_dealloc<kProducerRegs>();
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.q);
+      tma_prefetch_desc(&maps.vnew);
+      tma_prefetch_desc(&maps.vpool);
+    }
+    int jg = 0, itq0 = 0, itq1 = 0;
     ExtItem I;
     RingCursor rc;
     while (ring_pop(I, rc, ring, desc_full, desc_empty, lane == 0)) {
-      if (!is_v) {
-        const int qb = it & 1;
-        if (it >= 2) mbar_wait(q_empty + qb, ((it >> 1) - 1) & 1);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        if (I.n[x] == 0) continue;
+        int& itq = x ? itq1 : itq0;
+        if (itq > 0) mbar_wait(q_empty + x, (itq - 1) & 1);   // the previous item's last S_x retired
         if (lane == 0) {
-          mbar_arrive_expect_tx(q_full + qb, C::Q_BYTES);
-          ext_trace(p.trace, 1, it);
+          mbar_arrive_expect_tx(q_full + x, C::TILE_BYTES);
 #pragma unroll
           for (int c = 0; c < C::NCB; ++c)
-            tma_load_3d(sq + qb * C::Q_BYTES + c * 128 * kTileRowBytes, &maps.q, q_full + qb, c * 64, I.g * G,
-                        I.qo + I.t * TOK);
+            tma_load_3d(sq + x * C::TILE_BYTES + c * 128 * kTileRowBytes, &maps.q, q_full + x, c * 64, I.g * G,
+                        I.qo + (I.t0 + x) * TOK);
         }
+        ++itq;
       }
-      for (int j = 0; j < I.n_tiles; ++j, ++jg) {
-        const int st = jg % NS, rnd = jg / NS;
-        mbar_wait(empty + st, (rnd & 1) ^ 1);
-        if (lane == 0) ext_trace(p.trace, is_v ? 3 : 2, jg);
-        const uint32_t d = base_s + st * C::KV_BYTES;
-        // prefix tile: one 3-D TMA box when its 128 slots are consecutive, else a
-        // cp.async gather (see below); new-KV tile: one 3-D TMA box
-        bool tma = true;
-        int s0 = 0;
-        const int jt = I.tile0 + j;                     // absolute prefix tile (cascade chunks)
-        if (j < I.n_pre) {
-          const int base = jt * kBN + 4 * lane;
-          bool contig = true;
-          s0 = I.slots[jt * kBN];                       // (jt*kBN < P: the tile has >= 1 cached row)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) contig &= base + i < I.P && I.slots[base + i] == s0 + 4 * lane + i;
-          tma = __all_sync(0xffffffffu, contig);
-        }
-        if (tma) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(full + st, C::KV_BYTES);
-            if (j < I.n_pre) {
-#pragma unroll
-              for (int c = 0; c < C::NCB; ++c)
-                tma_load_3d(d + c * kBN * kTileRowBytes, m_pool, full + st, c * 64, I.g, s0);
-            } else {
-              const int nn = j - I.n_pre;
-#pragma unroll
-              for (int c = 0; c < C::NCB; ++c)
-                tma_load_3d(d + c * kBN * kTileRowBytes, m_new, full + st, c * 64, I.g, I.qo + nn * kBN);
-            }
-          } else {
-            mbar_arrive(full + st);
-          }
-        } else {
-          // Fragmented slots: per-lane 16-byte cp.async gathers written straight
-          // into the 128B-swizzled layout (chunk k of row r -> chunk k ^ (r & 7)).
-          // CPR lanes cover one pool row; rows past the prefix are zero-filled.
-          // (TMA tile::gather4 takes warp-uniform operands, which ptxas issues one
-          // lane at a time; this path keeps all 32 lanes issuing.)
-          constexpr int CPR = HD / 8, RPI = 32 / CPR;
-          const int ch = lane % CPR, rsub = lane / CPR;
-          const uint32_t dcol = d + (ch >> 3) * kBN * kTileRowBytes;
-          int slot_r[4];                                // slots of rows lane, lane+32, lane+64, lane+96
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int pos = jt * kBN + lane + 32 * i;
-            slot_r[i] = pos < I.P ? I.slots[pos] : -1;
-          }
-#pragma unroll
-          for (int rr = 0; rr < kBN; rr += RPI) {
-            const int row = rr + rsub;
-            const int sl = __shfl_sync(0xffffffffu, slot_r[rr / 32], row & 31);
-            const bool ok = sl > 0;
-            const __nv_bfloat16* src = base_g + (int64_t(ok ? sl : 0) * p.h_kv + I.g) * HD + ch * 8;
-            cp_async_16(dcol + row * kTileRowBytes + (((ch & 7) ^ (row & 7)) << 4), src, ok ? 16u : 0u);
-          }
-          cp_async_mbar_arrive_noinc(full + st);
-        }
+      const int N = max(I.n[0], I.n[1]);
+      for (int j = 0; j < N; ++j, ++jg) {
+        const int st = jg % C::VS, rnd = jg / C::VS;
+        const TileSrc t = probe_kv_tile(I, j, lane);
+        mbar_wait(v_empty + st, (rnd & 1) ^ 1);
+        load_kv_tile<HD>(I, j, t, sv_ + st * C::TILE_BYTES, v_full + st, &maps.vpool, &maps.vnew, p.vpool, p.h_kv,
+                         lane);
       }
-      ++it;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    // The whole warp walks the loop (converged, warp-uniform operands: see
-    // elect_one); one elected lane issues each tcgen05.mma / commit.
+    // The whole warp walks the loop (converged, warp-uniform operands); one elected lane issues
+    // each tcgen05.mma / commit.  Per K/V tile j and q tile x: O_x += P_x(j-1) V(j-1), then
+    // S_x(j) = Q_x K(j)^T — the ping-pong order (see the header).
+    regs_dealloc<kProducerRegs>();
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
-    int it = 0, jg = 0;
+    // Shared-memory descriptors are built once; advancing one by a byte offset inside the (< 227
+    // KB) shared window is an add of offset >> 4 to its 14-bit start-address field (no carry).
+    const uint64_t dq0 = umma_desc_sw128(sq, 16, 1024);                       // Q_x, K stages: K-major
+    const uint64_t dk0 = umma_desc_sw128(sk, 16, 1024);
+    const uint64_t dv0 = umma_desc_sw128(sv_, kBN * kTileRowBytes, 1024);     // V stages: MN-major
+    int jg = 0, jx0 = 0, jx1 = 0, itx0 = 0, itx1 = 0;
     ExtItem I;
     RingCursor rc;
     while (ring_pop(I, rc, ring, desc_full, desc_empty, lane == 0)) {
-      const int n_tiles = __shfl_sync(0xffffffffu, I.n_tiles, 0);   // uniform for ptxas
-      const int qb = it & 1;
-      const uint32_t qa = sq + qb * C::Q_BYTES;
-      const uint32_t t_o = tmem + C::O_COL + qb * HD;
-      mbar_wait(q_full + qb, (it >> 1) & 1);
-      if (it >= 2) mbar_wait(o_free + qb, ((it >> 1) - 1) & 1);  // epilogue of item it-2 read O[qb]
-      auto issue_s = [&](int j) {
-        const int g_ = jg + j;
-        const int st = g_ % C::KS;
-        if (lane == 0) ext_trace(p.trace, 15, g_);
-        mbar_wait(k_full + st, (g_ / C::KS) & 1);
-        if (lane == 0) ext_trace(p.trace, 11, g_);
-        tc_fence_after();
-        if (RX_FENCE) fence_proxy_async();   // cp.async (generic-proxy) writes -> visible to the MMA (async proxy)
-        const uint32_t kb = sk + st * C::KV_BYTES;
-        const uint32_t t_s = tmem + (g_ & 1) * 128;
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < HD / 16; ++k) {
-            const uint32_t off = (k >> 2) * 128 * kTileRowBytes + (k & 3) * 32;
-            umma_ss(t_s, umma_desc_sw128(qa + off, 16, 1024),
-                    umma_desc_sw128(kb + (k >> 2) * kBN * kTileRowBytes + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
-          }
-          ext_trace(p.trace, 13, g_);
-          tc_commit(s_full + (g_ & 1));
-          ext_trace(p.trace, 4, g_);
-          tc_commit(k_empty + st);                          // K_g is free once S_g retires
-          if (j == n_tiles - 1) tc_commit(q_empty + qb);    // last read of this Q buffer issued
+      const int n0 = __shfl_sync(0xffffffffu, I.n[0], 0);   // uniform for ptxas
+      const int n1 = __shfl_sync(0xffffffffu, I.n[1], 0);
+      const int N = max(n0, n1);
+      for (int j = 0; j <= N; ++j) {
+        const int kg = jg + j;                    // K tile j (global ring index)
+        if (j < N) {
+          mbar_wait(k_full + kg % C::KS, (kg / C::KS) & 1);
+          tc_fence_after();
+          fence_proxy_async();                    // cp.async (generic proxy) writes -> the MMA (async proxy)
         }
-        __syncwarp();
-      };
-      issue_s(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s(j + 1);
-        const int g_ = jg + j;
-        mbar_wait(p_full + (g_ & 1), (g_ >> 1) & 1);
-        if (lane == 0) ext_trace(p.trace, 5, g_);
-        tc_fence_after();
-        const int st = g_ % C::VS;
-        mbar_wait(v_full + st, (g_ / C::VS) & 1);
-        if (lane == 0) ext_trace(p.trace, 12, g_);
-        if (RX_FENCE) fence_proxy_async();
-        const uint32_t vb = sv_ + st * C::KV_BYTES;
-        const uint32_t t_p = tmem + (g_ & 1) * 128;
-        if (elect_one()) {
+        bool v_ready = false;
 #pragma unroll
-          for (int k = 0; k < kBN / 16; ++k)
-            umma_ts(t_o, t_p + k * 8, umma_desc_sw128(vb + k * 2048, kBN * kTileRowBytes, 1024), idesc_o,
-                    (j > 0 || k > 0) ? 1u : 0u);
-          ext_trace(p.trace, 14, g_);
-          tc_commit(v_empty + st);
-          tc_commit(o_done);
-          ext_trace(p.trace, 6, g_);
+        for (int x = 0; x < 2; ++x) {
+          const int nx = x ? n1 : n0;
+          if (nx == 0) continue;
+          const int jx = x ? jx1 : jx0;
+          const uint32_t t_s = tmem + x * 128;
+          if (j > 0 && j <= nx) {
+            // O_x += P_x(j-1) V(j-1), P read from TMEM (A operand), V from the ring
+            mbar_wait(p_full + x, (jx + j - 1) & 1);
+            const int vg = kg - 1;
+            if (!v_ready) {
+              mbar_wait(v_full + vg % C::VS, (vg / C::VS) & 1);
+              v_ready = true;
+              tc_fence_after();
+              fence_proxy_async();
+            } else {
+              tc_fence_after();
+            }
+            const uint64_t dv = dv0 + uint32_t(((vg % C::VS) * C::TILE_BYTES) >> 4);
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < kBN / 16; ++k)
+                umma_ts(tmem + C::O_COL + x * HD, t_s + k * 8, dv + uint32_t((k * 2048) >> 4), idesc_o,
+                        (j > 1 || k > 0) ? 1u : 0u);
+              if (j == nx) tc_commit(o_ready + x);        // O_x final for this item
+            }
+            __syncwarp();
+          }
+          if (j < nx) {
+            if (j == 0) {
+              mbar_wait(q_full + x, (x ? itx1 : itx0) & 1);
+              tc_fence_after();
+            }
+            const uint64_t dq = dq0 + uint32_t((x * C::TILE_BYTES) >> 4);
+            const uint64_t dk = dk0 + uint32_t(((kg % C::KS) * C::TILE_BYTES) >> 4);
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < HD / 16; ++k) {
+                const uint32_t off = uint32_t(((k >> 2) * 128 * kTileRowBytes + (k & 3) * 32) >> 4);
+                umma_ss(t_s, dq + off, dk + off, idesc_s, k > 0);
+              }
+              tc_commit(s_full + x);
+              if (j == nx - 1) tc_commit(q_empty + x);      // last read of Q_x issued
+            }
+            __syncwarp();
+          }
+        }
+        if (elect_one()) {
+          if (j < N) tc_commit(k_empty + kg % C::KS);       // K(j) free once both S(j) retire
+          if (j > 0) tc_commit(v_empty + (kg - 1) % C::VS);  // V(j-1) free once both P V(j-1) retire
         }
         __syncwarp();
       }
-      if (elect_one()) tc_commit(o_ready + qb);
-      __syncwarp();
-      jg += n_tiles;
-      ++it;
+      jg += N;
+      jx0 += n0;
+      jx1 += n1;
+      itx0 += n0 > 0;
+      itx1 += n1 > 0;
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax + epilogue
-    const int r = (warp - 4) * 32 + lane;          // row = TMEM lane
+    // ------------------------------------------------------------ softmax + epilogue of q tile x
+    regs_alloc<kSoftmaxRegs>();
+    const int x = (warp - 4) >> 2;
+    const int r = (warp & 3) * 32 + lane;          // row = TMEM lane
     const int i_tok = r / G, h = r % G;
-    const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
-    int it = 0, jg = 0;
+    const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + x * 128;
+    const uint32_t t_o = tmem + lane_off + C::O_COL + x * HD;
+    int jx = 0, itx = 0;
     ExtItem I;
     RingCursor rc;
     while (ring_pop(I, rc, ring, desc_full, desc_empty, lane == 0)) {
-      const int qb = it & 1;
-      const int rel = I.t * TOK + i_tok;           // position relative to prefix_len
+      const int nx = I.n[x];
+      if (nx == 0) continue;
+      const int rel = (I.t0 + x) * TOK + i_tok;     // position relative to prefix_len
       float m_ref = -INFINITY, l = 0.f;
-      for (int j = 0; j < I.n_tiles; ++j) {
-        const int g_ = jg + j;
-        const uint32_t t_s = tmem + lane_off + (g_ & 1) * 128;
-        mbar_wait(s_full + (g_ & 1), (g_ >> 1) & 1);
-        if (threadIdx.x == 128) ext_trace(p.trace, 7, g_);
+      for (int j = 0; j < nx; ++j, ++jx) {
+        mbar_wait(s_full + x, jx & 1);
         tc_fence_after();
         float sv[kBN];
 #pragma unroll
@@ -409,12 +523,11 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         // Scores stay raw (unscaled); the scale is folded into the exp2 FFMA.
         const int lim = j < I.n_pre ? I.P - (I.tile0 + j) * kBN - 1 : rel - (j - I.n_pre) * kBN;
         const bool full = __all_sync(0xffffffffu, lim >= kBN - 1);   // warp-uniform
-        // row max over 128 columns as 8 independent chains (one softmax warp per SM sub-partition:
-        // a single 64-deep FMNMX3 dependency chain would leave the SMSP idle on ALU latency)
         if (!full) {
 #pragma unroll
           for (int c = 0; c < kBN; ++c) sv[c] = c <= lim ? sv[c] : -INFINITY;
         }
+        // row max over 128 columns as 8 independent chains
         float mxp[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mxp[k] = fmaxf(sv[k], sv[k + 8]);
@@ -425,19 +538,12 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                          fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
         mx *= p.scale_log2;
-        // Lazy rescale, decided per WARP: tcgen05.ld/st are .sync.aligned
-        // warp-collective, so the O round trip must not diverge across rows.
-        // Lanes whose max did not grow get corr = 1.
+        // Lazy rescale, decided per WARP (tcgen05.ld/st are warp-collective).  S_x(j) retired,
+        // and it was issued after O_x += P_x(j-1) V(j-1), so O_x is complete up to j-1.
         if (__any_sync(0xffffffffu, mx > m_ref + 8.f) || j == 0) {
           const float m_new = fmaxf(mx, m_ref);
           const float corr = fast_exp2(m_ref - m_new);
           if (j > 0) {
-            // o_done completes once per P.V.  Having seen S_g complete, and since a
-            // tcgen05.commit tracks ALL prior MMAs of the issuer, P.V_{g-2} is done:
-            // completions are g-1 or g, so the parity wait for P.V_{g-1} is exact.
-            mbar_wait(o_done, (g_ - 1) & 1);
-            tc_fence_after();
-            const uint32_t t_o = tmem + lane_off + C::O_COL + qb * HD;
 #pragma unroll
             for (int c = 0; c < HD / 32; ++c) {
               float ov[32];
@@ -452,44 +558,29 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           l *= corr;
           m_ref = m_new;
         }
-        uint32_t pk[kBN / 2];
-        float rsp[4] = {0.f, 0.f, 0.f, 0.f};              // 4 independent row-sum chains
+        uint64_t rs[2] = {0ull, 0ull};                    // 2 packed (4 scalar) row-sum chains
         const float sc = p.scale_log2, nm = -m_ref;
         if (full) {
-          // MUFU ex2 is the softmax bottleneck (16/clk/SM vs 8192 MMA FLOP/clk):
-          // every 4th column is evaluated on the FMA pipe instead.
-#pragma unroll
-          for (int c = 0; c < kBN / 2; ++c) {
-            const float x0 = fmaf(sv[2 * c], sc, nm), x1 = fmaf(sv[2 * c + 1], sc, nm);
-            const float e0 = fast_exp2(x0);
-            const float e1 = (c & 1) ? exp2_poly3(x1) : fast_exp2(x1);
-            rsp[c & 3] += e0 + e1;
-            pk[c] = pack_bf16(e0, e1);
-          }
+          softmax_half<true>(sv, 0, sc, nm, rs, t_s);
+          softmax_half<true>(sv, 1, sc, nm, rs, t_s);
         } else {
-#pragma unroll
-          for (int c = 0; c < kBN / 2; ++c) {
-            const float e0 = fast_exp2(fmaf(sv[2 * c], sc, nm)), e1 = fast_exp2(fmaf(sv[2 * c + 1], sc, nm));
-            rsp[c & 3] += e0 + e1;
-            pk[c] = pack_bf16(e0, e1);
-          }
+          softmax_half<false>(sv, 0, sc, nm, rs, t_s);
+          softmax_half<false>(sv, 1, sc, nm, rs, t_s);
         }
-        l += (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
-        tmem_st32(t_s, pk);
-        tmem_st32(t_s + 32, pk + 32);
+        float r0, r1, r2, r3;
+        f2_unpack(rs[0], r0, r1);
+        f2_unpack(rs[1], r2, r3);
+        l += (r0 + r1) + (r2 + r3);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(p_full + (g_ & 1));
-        if (threadIdx.x == 128) ext_trace(p.trace, 8, g_);
+        mbar_arrive(p_full + x);
       }
-      // epilogue: O[qb] complete once this item's last P.V landed
-      mbar_wait(o_ready + qb, (it >> 1) & 1);
+      // epilogue: O_x complete once this item's last P V landed
+      mbar_wait(o_ready + x, itx & 1);
+      ++itx;
       if (p.pdl) pdl_wait();   // cascade partials: the previous step's merge must be done reading them
-      if (threadIdx.x == 128) ext_trace(p.trace, 9, it);
       tc_fence_after();
-      const uint32_t t_o = tmem + lane_off + C::O_COL + qb * HD;
       const float inv = 1.f / l;
-      __nv_bfloat16* orow = p.o + (int64_t(I.qo + rel) * p.h_q + I.g * G + h) * HD;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
         float ov[32];
@@ -506,6 +597,7 @@ __global__ void __launch_bounds__(kExtThreads, 1)
             if (c == 0) p.part_lse[pr] = m_ref + __log2f(l);
           }
         } else if (rel < I.ext) {
+          __nv_bfloat16* orow = p.o + (int64_t(I.qo + rel) * p.h_q + I.g * G + h) * HD;
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -518,47 +610,13 @@ __global__ void __launch_bounds__(kExtThreads, 1)
           }
         }
       }
+      // O_x is read: the next item's first P V into O_x is issued only after this warpgroup's
+      // next p_full arrival (the fence orders these TMEM reads before it)
       tc_fence_before();
-      mbar_arrive(o_free + qb);
-      if (threadIdx.x == 128) ext_trace(p.trace, 10, it);
-      jg += I.n_tiles;
-      ++it;
     }
-  } else if (warp == 2) {
-    // ------------------------------------------------------------ item scheduler (+ TMEM owner)
-    // (A5, storing the new K/V rows into their slots, is extend_store_kernel,
-    // launched just before this kernel on the same stream.)
-    // Items are handed out dynamically: a CTA takes the next work index when a descriptor slot is
-    // free (it runs kRing items ahead), so ragged batches (requests of different lengths: items of
-    // 1..N tiles, some q tiles absent) balance across SMs; consecutive indices still start at
-    // about the same time on neighbouring CTAs, which keeps one (b, g)'s prefix L2-resident.
-    RingCursor c;
-    for (;;) {
-      int w = 0;
-      if (lane == 0) w = atomicAdd(&p.sched[0], 1);
-      w = __shfl_sync(0xffffffffu, w, 0);
-      if (w >= W) break;
-      ExtItem I;
-      if (!ext_item<TOK>(p, qt, w, I)) continue;
-      mbar_wait(desc_empty + c.slot, c.phase ^ 1);
-      if (lane == 0) {
-        ring[c.slot] = I;
-        mbar_arrive(desc_full + c.slot);
-      }
-      __syncwarp();
-      if (++c.slot == kRing) {
-        c.slot = 0;
-        c.phase ^= 1;
-      }
-    }
-    mbar_wait(desc_empty + c.slot, c.phase ^ 1);      // sentinel
-    if (lane == 0) {
-      ExtItem I{};
-      I.b = -1;
-      ring[c.slot] = I;
-      mbar_arrive(desc_full + c.slot);
-    }
-    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ warp 2: TMEM owner only
+    regs_dealloc<kProducerRegs>();
   }
   tc_fence_before();
   __syncthreads();
@@ -650,11 +708,9 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   if (!p.sched) return cudaErrorInvalidValue;
   ExtendParams pp = p;
   pp.batch = batch;
-  static int trace_env = -1;
-  if (trace_env < 0) trace_env = getenv("RX_EXT_TRACE") ? 1 : 0;
-  pp.trace = trace_env;
   pp.max_qtiles = (max_ext + TOK - 1) / TOK;
-  const int64_t items = int64_t(pp.max_qtiles) * p.h_kv * (p.cascade ? p.n_kv_splits : batch);
+  const int64_t qpairs = (pp.max_qtiles + 1) / 2;
+  const int64_t items = qpairs * p.h_kv * (p.cascade ? p.n_kv_splits : batch);
   const int sms = device_sms();
   const int grid = int(items < sms ? items : sms);   // persistent: one CTA per SM
   if (p.pdl) {
@@ -698,14 +754,3 @@ cudaError_t launch_extend(int head_dim, int G, const ExtendParams& p, const void
 
 }  // namespace rx
 
-// Development only (not part of include/rx.h): copy and clear the extend-kernel
-// timeline ([16 codes][1024 items] clock64 values, 0 = not recorded) written
-// when RX_EXT_TRACE is set.  Returns the number of values copied.
-extern "C" int rx_debug_ext_trace(unsigned long long* out, int cap) {
-  const int n = 16 * 1024;
-  cudaDeviceSynchronize();
-  if (out && cap > 0) cudaMemcpyFromSymbol(out, rx::rx_ext_trace, sizeof(unsigned long long) * (n < cap ? n : cap));
-  static unsigned long long zero[16 * 1024];
-  cudaMemcpyToSymbol(rx::rx_ext_trace, zero, sizeof(zero));
-  return n < cap ? n : cap;
-}

@@ -115,7 +115,6 @@ struct ExtendParams {
   int part_splits;
   int part_base;
   int cas_prefix;               // shared prefix length (cascade mode; prefix_lens unused)
-  int trace;                    // development timeline tracer (RX_EXT_TRACE)
   // cascade partials launched as a programmatic dependent of the suffix decode: the grid may
   // start before that decode completes (it reads only the shared prefix); its epilogue waits for
   // the decode (hence the previous step's merge) before writing partials, and one thread per CTA

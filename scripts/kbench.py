@@ -37,6 +37,7 @@ def main():
     cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
     g = torch.Generator(device=dev).manual_seed(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ews = torch.zeros(1 << 20, dtype=torch.uint8, device=dev)     # zeroed workspace (rx.h header)
 
     def timeit(fn):
         for _ in range(3):
@@ -133,7 +134,7 @@ def main():
         ext = torch.from_numpy(Es.astype(np.int32)).to(dev)
         ind = torch.from_numpy(np.concatenate([[0], np.cumsum(Es)]).astype(np.int32)).to(dev)
         ms = timeit(lambda: rx.rx_extend(cfg, rtt, None, pre, ext, ind, N, int(Es.max()), int(Ps.max()), q, kn, vn,
-                                         kp, vp, o))
+                                         kp, vp, o, ews))
         flops = 4 * hd * h_q * float(np.sum(Es * Ps + Es * (Es + 1) / 2))
         print(f"extend {h_q}/{h_kv}/{hd} B={B} P~{a.prefix} E~{a.ext} ragged={a.ragged} half={a.half}: "
               f"{ms*1e3:.1f} us  {flops/ms/1e9:.1f} TFLOP/s tokens/s {N/ms*1e3:.3e}")
@@ -160,7 +161,7 @@ def main():
         pre = torch.full((B,), P, dtype=torch.int32, device=dev)
         ext = torch.full((B,), E, dtype=torch.int32, device=dev)
         ind = torch.arange(B + 1, dtype=torch.int32, device=dev) * E
-        ms = timeit(lambda: rx.rx_extend(cfg, rtt, None, pre, ext, ind, N, E, P, q, kn, vn, kp, vp, o))
+        ms = timeit(lambda: rx.rx_extend(cfg, rtt, None, pre, ext, ind, N, E, P, q, kn, vn, kp, vp, o, ews))
         flops = 4 * hd * h_q * B * (E * P + E * (E + 1) / 2)
         print(f"extend {h_q}/{h_kv}/{hd} B={B} P={P} E={E}: {ms*1e3:.1f} us  {flops/ms/1e9:.1f} TFLOP/s "
               f"tokens/s {N/ms*1e3:.3e}")
