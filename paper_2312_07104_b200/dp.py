@@ -37,6 +37,7 @@ class DPCluster:
             self.workers.append(e)
         self.assignments = []
         self.hint_min = 64
+        self.batches = [[] for _ in range(workers)]   # per worker: the request lists it ran, in order
 
     def run_batch(self, reqs, banks=None):
         """Dispatch one batch (router), run every worker's share (workers are independent: no
@@ -58,8 +59,11 @@ class DPCluster:
             lcp = _common_prefix([prompts[i] for i in idx])
             if len(sub) >= 2 and lcp >= self.hint_min:
                 from rxgen.workloads import Request
-                h = eng.run_batch([Request(prompts[idx[0]][:lcp].copy(), 0, f"hint-w{w}-{len(self.assignments)}")])[0]
+                hint = [Request(prompts[idx[0]][:lcp].copy(), 0, f"hint-w{w}-{len(self.assignments)}")]
+                self.batches[w].append(hint)
+                h = eng.run_batch(hint)[0]
                 self.router.rx_router_insert(w, h.tokens[:h.n_prompt])
+            self.batches[w].append(sub)
             out = eng.run_batch(sub)
             for i, r in zip(idx, out):
                 done[i] = r
