@@ -201,6 +201,39 @@ rx_status rx_schedule(rx_cache* c, int32_t batch, const int32_t* tokens, const i
 /* Pure queries (Alg. 1 "T.evictable_size() + P.available_size()", P:534;
  * SPEC S:149-156).  evictable = tokens on non-root nodes with ref 0 (pins
  * propagate to the root, so these are exactly the peelable nodes). */
+/* Alg. 1's output loop (§3) for PLAIN decoding — one new token per running
+ * request per iteration — planned on the host for up to max_steps iterations in one call (the
+ * generated tokens are inputs, so no iteration waits for the device).  Iteration k:
+ *   1. B = *n_running; if the next record does not fit in out (4·B words past those already used)
+ *      the call returns early;
+ *   2. alloc B slots (R6: on RX_E_NOMEM evict the shortfall B - rx_available and retry
+ *      once; RX_E_NOMEM again is returned and iteration k is not planned);
+ *   3. in batch order (R23) request b = running[j] gets slot j: table[b·stride + cur[b]] = slot,
+ *      cur[b] += 1, and the step's record [new slots | seq_lens (= new cur) | rows b | stable[b]]
+ *      (int32, B words each — the layout rx_decode_append takes from one staging buffer) is
+ *      written at out + step_meta[3k+1]; step_meta[3k] = B, step_meta[3k+2] = max seq_len;
+ *   4. every request with cur[b] == end[b] finishes: rx_dec_ref(nodes[b]) then
+ *      rx_insert(tokens[offsets[b] .. offsets[b] + end[b]), table row b) — batch order — and
+ *      leaves running (kept ascending, compacted in place).
+ * State (caller-owned host arrays, updated in place): table int32 [batch, stride] (the host mirror
+ * of req_to_token), cur int32 [batch], running int32 [*n_running] (ascending request indices).
+ * Inputs: end int32 [batch] (prompt + output length, <= stride, <= the request's token count),
+ * stable int32 [batch] (copied into records), nodes [batch] (pinned prefix nodes), tokens/offsets
+ * (int64 [batch+1]) the full token streams.  *n_steps = iterations planned.
+ * cb (nullable) reports the tree effects in order, vals as listed:
+ *   RX_EV_EVICT_RUN (slots of one evicted leaf), RX_EV_EVICT {short, evicted},
+ *   RX_EV_ALLOC {B} + slots, RX_EV_FINISH {b, d_evictable, new_cached, dup_freed}.
+ * Errors: RX_E_INVALID (null pointer, running not ascending / out of range, cur >= end, end past
+ * stride or tokens; checked before any effect); a tree error or RX_E_NOMEM stops the call after
+ * the iterations already planned (reported in *n_steps). */
+typedef enum { RX_EV_ALLOC = 0, RX_EV_EVICT_RUN = 1, RX_EV_EVICT = 2, RX_EV_FINISH = 3 } rx_step_event;
+typedef void (*rx_step_event_cb)(void* user, int32_t kind, const int64_t* vals, const int32_t* slots, int64_t n);
+rx_status rx_decode_steps(rx_cache* c, int32_t batch, int32_t* table, int64_t stride, int32_t* cur,
+                          const int32_t* end, const int32_t* stable, const rx_node* nodes, const int32_t* tokens,
+                          const int64_t* offsets, int32_t* running, int32_t* n_running, int32_t max_steps,
+                          int32_t* out, int64_t out_cap, int64_t* step_meta, int32_t* n_steps,
+                          rx_step_event_cb cb, void* user);
+
 int64_t rx_evictable_size(const rx_cache* c);
 int64_t rx_total_cached(const rx_cache* c);
 int64_t rx_available(const rx_cache* c);

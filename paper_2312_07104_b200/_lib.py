@@ -31,6 +31,7 @@ class AttnCfg(C.Structure):
 
 EVICT_CB = C.CFUNCTYPE(None, vp, P32, i64)
 EVICT_PATH_CB = C.CFUNCTYPE(None, vp, P32, i64, i64, P32, i64)
+STEP_EVENT_CB = C.CFUNCTYPE(None, vp, i32, P64, P32, i64)
 
 # symbol -> (restype, argtypes); the set of names is exactly include/rx.h's declarations
 SIGNATURES = {
@@ -61,6 +62,8 @@ SIGNATURES = {
     "rx_finish_batch": (C.c_int, [vp, i32, P64, P32, P64, P32, P64, P64, P64]),
     "rx_schedule": (C.c_int, [vp, i32, P32, P64, P64, i32, C.POINTER(C.c_uint64), P64, P64, P32, P32,
                               C.POINTER(i32), P64]),
+    "rx_decode_steps": (C.c_int, [vp, i32, P32, i64, P32, P32, P32, P64, P32, P64, P32, C.POINTER(i32), i32,
+                                  P32, i64, P64, C.POINTER(i32), STEP_EVENT_CB, vp]),
     "rx_fsm_create": (C.c_int, [C.c_char_p, i64, C.POINTER(vp)]),
     "rx_fsm_destroy": (None, [vp]),
     "rx_fsm_num_states": (i32, [vp]),

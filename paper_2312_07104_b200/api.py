@@ -13,7 +13,7 @@ import json
 
 import numpy as np
 
-from ._lib import lib, AttnCfg, EVICT_CB, EVICT_PATH_CB, RxError, P32, P64
+from ._lib import lib, AttnCfg, EVICT_CB, EVICT_PATH_CB, STEP_EVENT_CB, RxError, P32, P64
 
 _I32 = np.int32
 SCHED_POLICY = {"lspf": 0, "fcfs": 1, "random": 2}   # rx_sched_policy
@@ -149,6 +149,37 @@ class RadixCache:
         _check(lib.rx_inc_ref_batch(self._h, len(n), n.ctypes.data_as(P64), d.ctypes.data_as(P64)),
                "rx_inc_ref_batch")
         return d
+
+    def rx_decode_steps(self, table, cur, end, stable, nodes, tokens, offsets, running, n_running, max_steps,
+                        out, step_meta, events=None):
+        """Alg. 1 output loop for plain decoding (rx.h rx_decode_steps).  table / cur / running / out /
+        step_meta are updated IN PLACE (int32 C-contiguous; step_meta int64 [max_steps, 3]).
+        events: callable(kind, vals int64 array, slots int32 array) or None.
+        -> (status, n_steps, n_running); status 0 or RX_E_NOMEM (-2), other errors raise."""
+        for a, dt in ((table, _I32), (cur, _I32), (running, _I32), (out, _I32), (step_meta, np.int64)):
+            if a.dtype != dt or not a.flags.c_contiguous:
+                raise ValueError("rx_decode_steps: in-place arrays must be C-contiguous of the declared dtype")
+        if table.ndim != 2 or step_meta.size < 3 * max_steps:
+            raise ValueError("rx_decode_steps: table must be [batch, stride], step_meta >= 3 * max_steps")
+        e, st_, t = _i32(end), _i32(stable), _i32(tokens)
+        nd = np.ascontiguousarray(nodes, dtype=np.int64)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        nr, ns = C.c_int32(n_running), C.c_int32(0)
+        cb = None
+        if events is not None:
+            def relay(user, kind, vals, slots, n):
+                nv = {0: 1, 1: 0, 2: 2, 3: 4}[kind]
+                v = np.ctypeslib.as_array(vals, shape=(nv,)).copy() if nv else np.zeros(0, np.int64)
+                s = np.ctypeslib.as_array(slots, shape=(n,)).copy() if n else np.zeros(0, _I32)
+                events(kind, v, s)
+            cb = STEP_EVENT_CB(relay)
+        st = lib.rx_decode_steps(self._h, len(cur), _p32(table), table.shape[1], _p32(cur), _p32(e), _p32(st_),
+                                 nd.ctypes.data_as(P64), _p32(t), off.ctypes.data_as(P64), _p32(running),
+                                 C.byref(nr), max_steps, _p32(out), out.size, step_meta.ctypes.data_as(P64),
+                                 C.byref(ns), cb if cb is not None else STEP_EVENT_CB(), None)
+        if st not in (0, -2):
+            _check(st, "rx_decode_steps")
+        return st, ns.value, nr.value
 
     def rx_finish_batch(self, nodes, tokens_concat, offsets, slots_concat):
         """dec_ref + insert per request -> (d_evict, new_cached, dup_freed), each int64[B]"""

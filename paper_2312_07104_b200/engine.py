@@ -395,17 +395,98 @@ class Engine:
         self._finish_many(rs, np.nonzero(nseg == 0)[0], slots)
         running = np.nonzero(nseg > 0)[0]
         self.stats["tree_s"] += time.perf_counter() - t0
-        # Output phase, host ahead of the device.  (A) the tree ops of each step — its slots (R23:
-        # per step, in batch order), finished requests' dec_ref + insert — run on the host: none of
-        # it depends on GPU results (the mock-model tokens are known).  (B) every launch_chunk
-        # steps the planned steps are launched: runs of single-token steps as decode calls with ONE
-        # metadata H2D, multi-token (jump-forward) steps as extend calls — so the GPU starts on
-        # the phase while the host plans the rest of it.
+        # Output phase, host ahead of the device: the tree ops of each step — its slots (R23: per
+        # step, in batch order), finished requests' dec_ref + insert — need no GPU result (the
+        # mock-model tokens are known), so steps are planned in chunks and each chunk is launched
+        # while the host plans the next.
         cur = n_prompt + first
+        unit = all(r.first == 0 and (len(r.segs) == 0 or int(r.segs.max()) == 1) for r in rs)
+        if unit and self.on_decode_plan is None and self.evict_listener is None:
+            # Alg. 1's output loop in the library: one C call plans launch_chunk iterations (allocs,
+            # table rows, device staging records, finishes) — no per-step Python
+            self._decode_loop_native(rs, slots, cur, running, n_prompt + n_out)
+        else:
+            self._output_loop_py(rs, slots, cur, running, nseg, unit)
+        self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
+        return rs
+
+    def _decode_loop_native(self, rs, slots, cur, running, end):
+        """Plain decoding through rx_decode_steps: each C call plans launch_chunk iterations of
+        Alg. 1's output loop (alloc + evict-retry, table rows, finishes) and writes their device
+        staging records straight into a pinned buffer, which one H2D moves before the chunk's
+        decode launches."""
+        B = len(rs)
+        c = self.cache
+        t0 = time.perf_counter()
+        end = np.ascontiguousarray(end, dtype=np.int32)
+        cur32 = np.ascontiguousarray(cur, dtype=np.int32)
+        run = np.zeros(max(B, 1), dtype=np.int32)
+        nr = len(running)
+        run[:nr] = running
+        nodes = np.array([r.node for r in rs], dtype=np.int64)
+        tok_off = np.zeros(B + 1, dtype=np.int64)
+        tok_off[1:] = np.cumsum(end)
+        tokens = np.concatenate([r.tokens[:n] for r, n in zip(rs, end)])
+        collect = self.plan_only and self.collect_calls
+        hcat = np.concatenate([r.hashes[:n] for r, n in zip(rs, end)]) if collect else None
+        chunk = self.launch_chunk
+        meta = np.zeros((chunk, 3), dtype=np.int64)
+        events = self._step_events(rs) if self.record else None
+        self.stats["tree_s"] += time.perf_counter() - t0
+        while nr > 0:
+            t0 = time.perf_counter()
+            cap = 4 * nr * chunk
+            if self.plan_only:
+                stage, name = None, None
+                sn = np.empty(cap, dtype=np.int32)
+            else:
+                name = f"dec{self._ring % 4}"
+                self._ring += 1
+                stage = self._pinned(name, cap)
+                sn = stage.numpy()
+            st, ns, nr = c.rx_decode_steps(slots, cur32, end, self._stable, nodes, tokens, tok_off, run, nr, chunk,
+                                           sn, meta, events)
+            m = meta[:ns].copy()
+            self.stats["decode_tokens"] += int(m[:, 0].sum())
+            if collect:
+                for Bk, o, _ in m:
+                    rows, seq = sn[o + 2 * Bk:o + 3 * Bk], sn[o + Bk:o + 2 * Bk]
+                    self.calls.append(CallPlan("decode", hcat[tok_off[rows] + seq - 1], {"B": int(Bk)}))
+            self.stats["tree_s"] += time.perf_counter() - t0
+            if stage is not None:
+                if ns:
+                    self._decode_launch(stage[:int(m[-1, 1] + 4 * m[-1, 0])], name, m)
+                else:
+                    self._pinned_done(name)
+            if st != 0:
+                raise OutOfSlots(f"decode step needs {nr} slots, available {c.rx_available()}")
+
+    def _step_events(self, rs):
+        """rx_decode_steps event callback -> the same trace tuples as the Python path."""
+        runs = []
+
+        def ev(kind, v, s):
+            if kind == 1:
+                runs.append(tuple(int(x) for x in s))
+            elif kind == 2:
+                self._rec("evict", int(v[0]), int(v[1]), tuple(runs))
+                runs.clear()
+            elif kind == 0:
+                self._rec("alloc", int(v[0]), tuple(int(x) for x in s))
+            else:
+                b = int(v[0])
+                self._rec("dec_ref", rs[b].rid, int(v[1]))
+                self._rec("insert", rs[b].rid, int(v[2]), int(v[3]))
+        return ev
+
+    def _output_loop_py(self, rs, slots, cur, running, nseg, unit):
+        """Output phase in Python: jump-forward segments (FSM workload), DP workers (evictions go to
+        the router as token paths) and the on_decode_plan hook.  Host ahead of the device: the tree
+        ops of each step run on the host (none depends on GPU results), and every launch_chunk
+        steps the planned steps are launched (runs of single-token steps as decode calls with ONE
+        metadata H2D, multi-token steps as extend calls)."""
         step = 0
         steps = []
-        # plain decoding (every segment one token): no per-request Python per step
-        unit = all(r.first == 0 and (len(r.segs) == 0 or int(r.segs.max()) == 1) for r in rs)
         while len(running):
             t0 = time.perf_counter()
             if unit:
@@ -441,8 +522,6 @@ class Engine:
                 steps = []
         if steps and not self.plan_only:
             self._launch_steps(rs, slots, steps)
-        self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
-        return rs
 
     def _launch_steps(self, rs, slots, steps):
         """Launch planned output steps in order: runs of decode steps share one metadata H2D."""
@@ -622,26 +701,35 @@ class Engine:
         return [(edges[i], edges[i + 1]) for i in range(len(edges) - 1)] if len(edges) > 2 else None
 
     def _decode_phase(self, steps):
-        """Launch a batch's decode steps: one H2D of [new_slots | seq_lens | rows] for every step,
-        then one rx_decode_append (or rx_decode_cascade_append) per step."""
-        dev = self.device
+        """Launch a batch's decode steps planned in Python: their records [new slots | seq_lens | rows
+        | stable lens] in one pinned staging buffer (the rx_decode_steps layout), then _decode_launch."""
         offs = np.zeros(len(steps) + 1, dtype=np.int64)
         offs[1:] = np.cumsum([4 * len(r) for r, _, _ in steps])
         name = f"dec{self._ring % 4}"
         self._ring += 1
         stage = self._pinned(name, int(offs[-1]))
         sn = stage.numpy()
-        need = 0
-        sh = self._shared
-        for (running, new, pos), o0 in zip(steps, offs):
+        meta = np.zeros((len(steps), 3), dtype=np.int64)
+        for k, ((running, new, pos), o0) in enumerate(zip(steps, offs)):
             B = len(running)
             sn[o0:o0 + B] = new
             sn[o0 + B:o0 + 2 * B] = pos + 1             # seq_len counts the new token
             sn[o0 + 2 * B:o0 + 3 * B] = running         # table row of each running request
             sn[o0 + 3 * B:o0 + 4 * B] = self._stable[running]   # written by the batch's prefill
-            ms = int(pos.max()) + 1
-            need = max(need, api.rx_decode_cascade_workspace_bytes(self.cfg, B, ms, sh) if sh
-                       else api.rx_decode_workspace_bytes(self.cfg, B, ms))
+            meta[k] = (B, o0, int(pos.max()) + 1)
+        self._decode_launch(stage, name, meta)
+
+    def _decode_launch(self, stage, name, meta):
+        """One H2D of the staged step records, then one rx_decode_append (or
+        rx_decode_cascade_append) per step.  meta[k] = (B, word offset, max seq_len)."""
+        dev = self.device
+        sh = self._shared
+        need = 0
+        for B, _, ms in meta:
+            need = max(need, api.rx_decode_cascade_workspace_bytes(self.cfg, int(B), int(ms), sh) if sh
+                       else api.rx_decode_workspace_bytes(self.cfg, int(B), int(ms)))
+        # decode_bytes() needs (running, pos) per call, read after the timed region: copy the records
+        sn = stage.numpy().copy() if self.timer is not None else None
         d_all = stage.to(dev, non_blocking=True)
         self._pinned_done(name)
         if need > self._ws.numel():
@@ -652,12 +740,11 @@ class Engine:
         per_call = self.gather is not None
         ev_run = None if per_call else self._tbeg()
         works, nl_run = [], 0
-        for (running, new, pos), o0 in zip(steps, offs):
-            B = len(running)
+        for B, o0, max_seq in meta:
+            B, o0, max_seq = int(B), int(o0), int(max_seq)
             q, k, v = self.bank.dec[self._dec_i]
             self._dec_i += 1
             d = d_all[o0:o0 + 4 * B]
-            max_seq = int(pos.max()) + 1
             o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
             ev0 = self._tbeg() if per_call else None
             if sh:
@@ -670,11 +757,13 @@ class Engine:
                                      self.k_pool, self.v_pool, o, self._ws, stable_lens=d[3 * B:])
             nl = api.rx_last_launch_count()
             self.stats["launches"] += nl
-            # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot indices,
-            # computed after the timed region from (slots, running, pos)
-            if ev0 is not None:
-                self._tend(ev0, "decode", [(self._slots_host, running, pos)], nl)
-            works.append((self._slots_host, running, pos))
+            if sn is not None:
+                # algorithmic bytes: distinct pool rows read (K+V) + q + o + slot
+                # indices, computed after the timed region from (slots, running, pos)
+                w = (self._slots_host, sn[o0 + 2 * B:o0 + 3 * B].astype(np.int64), sn[o0 + B:o0 + 2 * B] - 1)
+                if ev0 is not None:
+                    self._tend(ev0, "decode", [w], nl)
+                works.append(w)
             nl_run += nl
             if self.gather is not None:
                 o = self.gather(o)
@@ -683,7 +772,7 @@ class Engine:
             if self.keep_outputs:
                 self.outputs.append(("decode", o, {"B": B}))
         if ev_run is not None:
-            self._tend(ev_run, "decode", works, nl_run, calls=len(steps))
+            self._tend(ev_run, "decode", works, nl_run, calls=len(meta))
 
     # ------------------------------------------------------------------ pinned staging
     def _pinned(self, name, n):

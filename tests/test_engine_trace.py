@@ -99,3 +99,48 @@ def test_ragged_flat_matches_loop():
         lens = rng.integers(0, 9, n)
         ref = np.concatenate([np.arange(s, s + l) for s, l in zip(starts, lens)]) if n else np.zeros(0)
         assert np.array_equal(_ragged_flat(starts, lens), ref.astype(np.int64))
+
+
+def _decode_evicting_workload(num_slots=420):
+    """Earlier phases leave ref-0 cache; a later batch's DECODE steps run the free pool dry, so the
+    per-step alloc of rx_decode_steps must evict (R6) mid-phase."""
+    from rxgen.workloads import Workload, Request, Shape
+    rng = np.random.default_rng(9)
+    phases = []
+    for ph in range(3):
+        pre = rng.integers(1, 30000, 60).astype(np.int32)
+        reqs = [Request(np.concatenate([pre, rng.integers(1, 30000, 10).astype(np.int32)]), int(rng.integers(20, 40)),
+                        f"p{ph}r{i}") for i in range(4)]
+        phases.append(("batch", reqs))
+    return Workload("DEV", Shape(8, 2, 64), num_slots, 32000, 9, phases)
+
+
+def test_decode_steps_evict_mid_phase():
+    """rx_decode_steps (Alg. 1's output loop in C++) under memory pressure: evictions happen between
+    a phase's decode steps, and the trace equals the oracle's entry for entry."""
+    o, e = _traces(_decode_evicting_workload())
+    ev_in_decode = [i for i, t in enumerate(o) if t[0] == "evict" and i > 0 and o[i + 1][0] == "alloc"
+                    and o[i + 1][1] <= 4]
+    assert ev_in_decode, "the workload must evict inside a decode phase"
+    _cmp(o, e)
+
+
+@pytest.mark.parametrize("cfg", [
+    lambda: workloads.c3(sessions=10, turns=3, in_lo=5, in_hi=30, out_lo=3, out_hi=12, num_slots=8192),
+    lambda: workloads.c4(),
+    _decode_evicting_workload,
+])
+def test_native_decode_loop_equals_python_loop(cfg):
+    """The C++ decode-step planner and the Python output loop (still used for jump-forward segments,
+    DP workers and the on_decode_plan hook) produce the same trace and the same per-call row hashes."""
+    wl = cfg()
+    a = Engine(wl, plan_only=True, record=True)
+    a.run_workload()
+    b = Engine(wl, plan_only=True, record=True)
+    b.on_decode_plan = lambda *args: None           # forces the Python loop
+    b.run_workload()
+    _cmp(a.trace, b.trace)
+    assert len(a.calls) == len(b.calls)
+    for x, y in zip(a.calls, b.calls):
+        assert x.kind == y.kind and np.array_equal(x.hashes, y.hashes)
+    assert a.stats["decode_tokens"] == b.stats["decode_tokens"]
