@@ -18,8 +18,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "librx.so")
+BUILD = os.path.join(HERE, "build", "obj_" + os.path.basename(os.environ["RX_LIB_OUT"])) if os.environ.get("RX_LIB_OUT") \
+    else os.path.join(HERE, "build")
+LIB = os.environ.get("RX_LIB_OUT") or os.path.join(HERE, "librx.so")   # RX_LIB_OUT: A/B variant builds
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

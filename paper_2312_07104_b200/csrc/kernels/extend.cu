@@ -218,16 +218,25 @@ __device__ __forceinline__ void load_kv_tile(const ExtItem& I, int j, const Tile
       mbar_arrive(full);
     }
   } else {
-    constexpr int CPR = HD / 8, RPI = 32 / CPR;
-    const int ch = lane % CPR, rsub = lane / CPR;
-    const uint32_t dcol = d + (ch >> 3) * kBN * kTileRowBytes;
+    // lane pair (2k, 2k+1) owns rows k + 16 i (i = 0..7), lane parity picks the 16-byte chunks of
+    // a row: one warp instruction moves 16 rows x 32 contiguous bytes (whole sectors), and per row
+    // a lane computes one source and one destination base — the 16-byte pieces of a row go out
+    // with immediate source offsets (a tile is ~160 instructions per warp, not ~1700)
+    constexpr int CPR = HD / 8;                       // 16-byte chunks per row
+    const int par = lane & 1, rl = lane >> 1;
+    const int kx = (rl & 7) ^ par;                    // swizzle: chunk c of row r -> c ^ (r & 7)
 #pragma unroll
-    for (int rr = 0; rr < kBN; rr += RPI) {
-      const int row = rr + rsub;
-      const int sl = __shfl_sync(0xffffffffu, t.slot_r[rr / 32], row & 31);
+    for (int i = 0; i < kBN / 16; ++i) {
+      const int row = rl + 16 * i;                    // (row & 7) == (rl & 7)
+      const int sl = __shfl_sync(0xffffffffu, t.slot_r[i >> 1], rl + 16 * (i & 1));
       const bool ok = sl > 0;
-      const __nv_bfloat16* src = base_g + (int64_t(ok ? sl : 0) * h_kv + I.g) * HD + ch * 8;
-      cp_async_16(dcol + row * kTileRowBytes + (((ch & 7) ^ (row & 7)) << 4), src, ok ? 16u : 0u);
+      const char* src = reinterpret_cast<const char*>(base_g + (int64_t(ok ? sl : 0) * h_kv + I.g) * HD) + par * 16;
+      const uint32_t drow = d + row * kTileRowBytes;
+#pragma unroll
+      for (int m = 0; m < CPR / 2; ++m) {             // chunk c = 2m + par
+        const uint32_t dst = drow + ((2 * m) >> 3) * kBN * kTileRowBytes + ((((2 * m) & 7) ^ kx) << 4);
+        cp_async_16(dst, src + 32 * m, ok ? 16u : 0u);
+      }
     }
     cp_async_mbar_arrive_noinc(full);
   }
