@@ -419,8 +419,8 @@ rx_status rx_extend(const rx_attn_cfg* cfg, int32_t batch,
  * slots of positions < shared_len equal in every row (not checked); when
  * shared_len == 0 or the multi-query shape condition of rx_extend fails the
  * call is exactly rx_extend.  Workspace: >= rx_extend_cascade_workspace_bytes
- * (cfg, total_new, shared_len) bytes.  Four launches (store, suffix, shared,
- * merge). */
+ * (cfg, total_new, shared_len) bytes.  Four launches (store, suffix partial,
+ * shared prefix stream-K, log-sum-exp merge). */
 size_t rx_extend_cascade_workspace_bytes(const rx_attn_cfg* cfg, int64_t total_new, int32_t shared_len);
 rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t* d_rtt, int64_t rtt_stride,
                             const int32_t* d_rows, const int32_t* d_prefix_lens, const int32_t* d_extend_lens,
@@ -474,10 +474,11 @@ size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t 
  * rx_decode_append, but positions [0, shared_len), which must hold the SAME
  * slots in every batch row (a radix node all requests are pinned on; the slots
  * of row d_rows[0] are read), are attended ONCE for the whole batch as a dense
- * tensor-core problem (rows = requests x GQA heads, split over the prefix),
- * each request's suffix [shared_len, seq_len) by the decode kernel, and the
- * partials merged by log-sum-exp.  Requires 0 <= shared_len < every seq_len
- * (shared_len == 0 falls back to rx_decode_append).  3 launches.
+ * tensor-core problem (rows = requests x GQA heads; the (q-tile pair, kv head)
+ * x prefix-tile work split stream-K over the SMs), each request's suffix
+ * [shared_len, seq_len) by the decode kernel first, and the partials merged by
+ * log-sum-exp.  Requires 0 <= shared_len < every seq_len (shared_len == 0
+ * falls back to rx_decode_append).  3 launches (suffix, shared, merge).
  * Workspace: rx_decode_cascade_workspace_bytes(cfg, batch, max_seq_len, shared_len). */
 rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch,
                                    int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rows,

@@ -203,32 +203,34 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   int launches = 0;
   cudaError_t e = rx::launch_decode(cfg->head_dim, G, dp, batch, st, &launches);
   if (e != cudaSuccess) return RX_E_CUDA;
-  // (2) shared prefix [0, shared_len), attended ONCE for all requests on the
-  //     tensor cores (rows = requests x GQA heads): partials at splits [0, n_sh)
+  // (2) shared prefix [0, shared_len), attended ONCE for all requests on the tensor cores (rows =
+  //     requests x GQA heads), stream-K over the SMs: partials at [0, n_sh); (3) the log-sum-exp
+  //     merge with (1)'s suffix partials into o
   rx::ExtendParams ep{};
   ep.rtt = d_rtt;
   ep.rtt_stride = rtt_stride;
   ep.rows = d_rows;
   ep.kpool = static_cast<__nv_bfloat16*>(d_k_pool);
   ep.vpool = static_cast<__nv_bfloat16*>(d_v_pool);
+  ep.o = static_cast<__nv_bfloat16*>(d_o);
   ep.h_q = cfg->h_q;
   ep.h_kv = cfg->h_kv;
   ep.num_slots = num_slots;
   ep.scale_log2 = scale_log2;
   ep.cascade = 1;
-  ep.kv_split_tiles = pl.kv_split_tiles;
-  ep.n_kv_splits = pl.n_sh;
+  ep.cas_ctas = pl.ctas;
+  ep.cas_tiles = pl.tiles;
+  ep.n_sh = pl.n_sh;
   ep.part_o = ws_o;
   ep.part_lse = ws_lse;
   ep.part_splits = pl.total_splits;
-  ep.part_base = 0;
   ep.cas_prefix = shared_len;
+  ep.cas_seq_lens = d_seq_lens;
+  ep.cas_kv_start = shared_len;
+  ep.cas_chunk = pl.suffix.chunk;
   ep.pdl = rx::pdl_on();
   ep.sched = static_cast<int*>(d_ws);
   e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, batch, st);
-  if (e != cudaSuccess) return RX_E_CUDA;
-  // (3) log-sum-exp merge of shared + suffix partials
-  e = rx::launch_decode_merge(cfg->head_dim, dp, batch, st);
   if (e != cudaSuccess) return RX_E_CUDA;
   g_last_launches = launches + 2;
   return RX_OK;
@@ -304,34 +306,33 @@ rx_status rx_extend_cascade(const rx_attn_cfg* cfg, int32_t batch, const int32_t
   dp.col_tiles = (max_extend_len * G + 7) / 8;
   dp.kv_start = shared_len;
   dp.split_base = pl.n_sh;
-  dp.fixed_splits = pl.total_splits;
   e = rx::launch_decode_multi(cfg->head_dim, G, dp, batch, st);
   if (e != cudaSuccess) return RX_E_CUDA;
   // (2) the shared prefix [0, shared_len) once for every row of the batch on tcgen05 (the rows are
-  //     one virtual request, no mask: every row's position is >= shared_len): splits [0, n_sh)
+  //     one virtual request, no mask: every row's position is >= shared_len), stream-K; (3) the
+  //     log-sum-exp merge with (1)'s partial into o
   rx::ExtendParams ep{};
   ep.rtt = d_rtt;
   ep.rtt_stride = rtt_stride;
   ep.rows = d_rows;
   ep.kpool = static_cast<__nv_bfloat16*>(d_k_pool);
   ep.vpool = static_cast<__nv_bfloat16*>(d_v_pool);
+  ep.o = static_cast<__nv_bfloat16*>(d_o);
   ep.h_q = cfg->h_q;
   ep.h_kv = cfg->h_kv;
   ep.num_slots = num_slots;
   ep.scale_log2 = scale_log2;
   ep.cascade = 1;
-  ep.kv_split_tiles = pl.kv_split_tiles;
-  ep.n_kv_splits = pl.n_sh;
+  ep.cas_ctas = pl.ctas;
+  ep.cas_tiles = pl.tiles;
+  ep.n_sh = pl.n_sh;
   ep.part_o = ws_o;
   ep.part_lse = ws_lse;
   ep.part_splits = pl.total_splits;
-  ep.part_base = 0;
   ep.cas_prefix = shared_len;
+  ep.cas_fixed_suffix = 1;
   ep.sched = static_cast<int*>(d_ws);
   e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, int(total_new), st);
-  if (e != cudaSuccess) return RX_E_CUDA;
-  // (3) log-sum-exp merge per row
-  e = rx::launch_decode_merge(cfg->head_dim, dp, int(total_new), st);
   if (e != cudaSuccess) return RX_E_CUDA;
   g_last_launches = 4;
   return RX_OK;

@@ -337,8 +337,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const De
   const int64_t pair = int64_t(blockIdx.x) * kMergeWarps + (threadIdx.x >> 5);
   if (pair >= int64_t(rows) * p.h_q) return;
   const int b = int(pair / p.h_q);
-  const int nsplit = p.fixed_splits > 0 ? p.fixed_splits
-                                        : p.split_base + (p.seq_lens[b] - p.kv_start + p.chunk - 1) / p.chunk;
+  const int nsplit = p.split_base + (p.seq_lens[b] - p.kv_start + p.chunk - 1) / p.chunk;
   if (nsplit <= 1) return;
   const int64_t base = pair * p.max_splits;
   float M = -INFINITY;
@@ -453,13 +452,6 @@ cudaError_t launch_decode_multi(int head_dim, int G, const DecodeParams& p, int 
   RX_DEC_CASE(128, 1) RX_DEC_CASE(128, 2) RX_DEC_CASE(128, 4) RX_DEC_CASE(128, 8)
 #undef RX_DEC_CASE
   return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st) {
-  // PDL: the merge waits (griddepcontrol.wait) for the preceding grid before reading partials
-  if (head_dim == 64)
-    return launch_pdl(decode_merge_kernel<64>, merge_grid(batch, p.h_q), dim3(kMergeWarps * 32), 0, st, p, batch);
-  return launch_pdl(decode_merge_kernel<128>, merge_grid(batch, p.h_q), dim3(kMergeWarps * 32), 0, st, p, batch);
 }
 
 // Pipeline depth per warp for head_dim 128: 2 (default: 64 KB smem, 3 CTAs/SM;

@@ -86,8 +86,9 @@ static_assert(ExtCfg<128>::SMEM <= 232448, "extend kernel exceeds the 227 KB opt
 struct ExtItem {
   int b, g, t0, P, ext, qo, n_pre;
   int n[2];
-  int tile0;            // first prefix tile (cascade chunk), 0 otherwise
-  int split;            // cascade chunk index
+  int tile0;            // first prefix tile (cascade segment), 0 otherwise
+  int split;            // cascade: segment number within its unit (= partial index)
+  int unit;             // cascade: (q-tile pair, kv head) unit
   const int32_t* slots;
 };
 
@@ -121,28 +122,9 @@ __device__ __forceinline__ bool ext_item(const ExtendParams& p, int qp, int w, E
   // and re-served from L2.
   const int pair = qp - 1 - w % qp;
   it.t0 = 2 * pair;
-  if (p.cascade) {
-    // (kv head, prefix chunk) outer: all q tiles of one chunk share its K/V through L2.
-    // One virtual request (b = 0) of `batch` rows; no mask except the prefix end.
-    const int gs = w / qp;
-    it.g = gs % p.h_kv;
-    it.split = gs / p.h_kv;
-    it.b = 0;
-    it.ext = p.batch;
-    if (it.t0 * TOK >= it.ext) return false;
-    it.P = p.cas_prefix;
-    it.qo = 0;
-    const int row = p.rows ? p.rows[0] : 0;
-    it.slots = p.rtt + int64_t(row) * p.rtt_stride;
-    const int total = (it.P + kBN - 1) / kBN;
-    it.tile0 = it.split * p.kv_split_tiles;
-    it.n_pre = min(p.kv_split_tiles, total - it.tile0);
-    it.n[0] = it.n_pre;
-    it.n[1] = (it.t0 + 1) * TOK < it.ext ? it.n_pre : 0;
-    return it.n_pre > 0;
-  }
   it.tile0 = 0;
   it.split = 0;
+  it.unit = 0;
   const int bg = w / qp;
   it.g = bg % p.h_kv;
   it.b = bg / p.h_kv;
@@ -160,6 +142,31 @@ __device__ __forceinline__ bool ext_item(const ExtendParams& p, int qp, int w, E
     it.n[x] = t * TOK < it.ext ? it.n_pre + (rel_end + kBN - 1) / kBN : 0;
   }
   return true;
+}
+
+// Cascade (shared-prefix) segment: pair-tiles [x, xe) of virtual CTA c, cut at the end of unit
+// u = x / tiles (kv head major: u = g * qp + pair).  Returns the end of the segment.
+template <int TOK>
+__device__ __forceinline__ int64_t cas_segment(const ExtendParams& p, int qp, int c, int64_t x, int64_t xe,
+                                               int64_t W, ExtItem& it) {
+  const int T = p.cas_tiles;
+  const int u = int(x / T);
+  const int64_t end = min(xe, int64_t(u + 1) * T);
+  it.unit = u;
+  it.g = u / qp;
+  it.t0 = 2 * (u % qp);
+  it.b = 0;
+  it.ext = p.batch;
+  it.P = p.cas_prefix;
+  it.qo = 0;
+  const int row = p.rows ? p.rows[0] : 0;
+  it.slots = p.rtt + int64_t(row) * p.rtt_stride;
+  it.tile0 = int(x - int64_t(u) * T);
+  it.n_pre = int(end - x);
+  it.n[0] = it.n_pre;
+  it.n[1] = (it.t0 + 1) * TOK < it.ext ? it.n_pre : 0;
+  it.split = c - cas_cta_of(int64_t(u) * T, W, p.cas_ctas);
+  return end;
 }
 
 // Where the rows of K/V tile j of item I come from, resolved BEFORE the producer waits for a free
@@ -296,7 +303,8 @@ __global__ void __launch_bounds__(kExtThreads, 1)
   ExtItem* ring = reinterpret_cast<ExtItem*>(smem + C::SMEM_DATA + 512);
 
   const int qp = (p.max_qtiles + 1) / 2;              // q-tile pairs per (b, g)
-  const int W = p.cascade ? qp * p.h_kv * p.n_kv_splits : qp * p.h_kv * p.batch;
+  const int W = qp * p.h_kv * p.batch;                // work indices (non-cascade)
+  const int64_t Wc = int64_t(qp) * p.h_kv * p.cas_tiles;   // cascade pair-tiles
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -355,7 +363,21 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         c.phase ^= 1;
       }
     };
+    int cas_c = -1;                     // cascade: current virtual CTA and its remaining range
+    int64_t cas_x = 0, cas_xe = 0;
     auto next = [&](ExtItem& it) -> bool {
+      if (p.cascade) {
+        if (cas_x >= cas_xe) {
+          int c = 0;
+          if (lane == 0) c = atomicAdd(&p.sched[0], 1);
+          cas_c = __shfl_sync(0xffffffffu, c, 0);
+          if (cas_c >= p.cas_ctas) return false;
+          cas_x = cas_cut(cas_c, Wc, p.cas_ctas);
+          cas_xe = cas_cut(cas_c + 1, Wc, p.cas_ctas);
+        }
+        cas_x = cas_segment<TOK>(p, qp, cas_c, cas_x, cas_xe, Wc, it);
+        return true;
+      }
       for (;;) {
         int w = 0;
         if (lane == 0) w = atomicAdd(&p.sched[0], 1);
@@ -596,9 +618,9 @@ __global__ void __launch_bounds__(kExtThreads, 1)
         tmem_ld32(t_o + c * 32, ov);
         tmem_ld_wait();
         if (p.cascade) {
-          // partial over this prefix chunk: normalized fp32 o + log2-domain lse
+          // partial over this segment: normalized fp32 o + log2-domain lse
           if (rel < I.ext) {
-            const int64_t pr = (int64_t(rel) * p.h_q + I.g * G + h) * p.part_splits + p.part_base + I.split;
+            const int64_t pr = (int64_t(rel) * p.h_q + I.g * G + h) * p.part_splits + I.split;
             float4* dst = reinterpret_cast<float4*>(p.part_o + pr * HD + c * 32);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
@@ -719,7 +741,7 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   pp.batch = batch;
   pp.max_qtiles = (max_ext + TOK - 1) / TOK;
   const int64_t qpairs = (pp.max_qtiles + 1) / 2;
-  const int64_t items = qpairs * p.h_kv * (p.cascade ? p.n_kv_splits : batch);
+  const int64_t items = p.cascade ? int64_t(p.cas_ctas) : qpairs * p.h_kv * batch;
   const int sms = device_sms();
   const int grid = int(items < sms ? items : sms);   // persistent: one CTA per SM
   if (p.pdl) {
@@ -739,11 +761,85 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
   return cudaPeekAtLastError();
 }
 
+// Log-sum-exp merge of the cascade partials (A8): row `row`, q head hq (one warp, lanes over the
+// head dims) combines its unit's stream-K segment partials [0, parts) and its suffix partials
+// [n_sh, n_sh + ns) into bf16 o.  Launched right after the shared-prefix pass (programmatic
+// dependent: it waits for that grid, and through it for the suffix kernel, before reading).
+constexpr int kCasMergeWarps = 8;
+
+template <int HD>
+__global__ void __launch_bounds__(kCasMergeWarps * 32) cascade_merge_kernel(const ExtendParams p, int rows, int G) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t pair = int64_t(blockIdx.x) * kCasMergeWarps + (threadIdx.x >> 5);
+  if (pair >= int64_t(rows) * p.h_q) return;
+  const int row = int(pair / p.h_q), hq = int(pair % p.h_q);
+  const int tok = 128 / G;
+  const int qp = (p.max_qtiles + 1) / 2;
+  const int unit = (hq / G) * qp + (row / tok) / 2;
+  const int64_t Wc = int64_t(qp) * p.h_kv * p.cas_tiles;
+  const int parts = cas_parts(unit, p.cas_tiles, Wc, p.cas_ctas);
+  const int ns = p.cas_fixed_suffix > 0 ? p.cas_fixed_suffix
+                                        : (p.cas_seq_lens[row] - p.cas_kv_start + p.cas_chunk - 1) / p.cas_chunk;
+  const int nk = parts + ns;
+  const int64_t base = pair * p.part_splits;
+  auto idx = [&](int k) { return k < parts ? k : p.n_sh + (k - parts); };
+  float M = -INFINITY;
+  for (int k = lane; k < nk; k += 32) M = fmaxf(M, p.part_lse[base + idx(k)]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  constexpr int V = HD / 32;                       // 4 (hd 128) or 2 (hd 64) floats per lane
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  float W = 0.f;
+#pragma unroll 4
+  for (int k = 0; k < nk; ++k) {
+    const int64_t pr = base + idx(k);
+    const float w = fast_exp2(p.part_lse[pr] - M);
+    W += w;
+    const float* src = p.part_o + pr * HD + lane * V;
+    if constexpr (V == 4) {
+      const float4 x = *reinterpret_cast<const float4*>(src);
+      acc[0] += w * x.x, acc[1] += w * x.y, acc[2] += w * x.z, acc[3] += w * x.w;
+    } else {
+      const float2 x = *reinterpret_cast<const float2*>(src);
+      acc[0] += w * x.x, acc[1] += w * x.y;
+    }
+  }
+  const float inv = 1.f / W;
+  __nv_bfloat16* dst = p.o + pair * HD + lane * V;
+#pragma unroll
+  for (int v = 0; v < V; v += 2) *reinterpret_cast<uint32_t*>(dst + v) = pack_bf16(acc[v] * inv, acc[v + 1] * inv);
+}
+
+template <int HD>
+static cudaError_t launch_cascade_merge(const ExtendParams& p, int rows, int G, cudaStream_t st) {
+  ExtendParams pp = p;
+  pp.max_qtiles = (rows + 128 / G - 1) / (128 / G);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned((int64_t(rows) * p.h_q + kCasMergeWarps - 1) / kCasMergeWarps));
+  cfg.blockDim = dim3(kCasMergeWarps * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, cascade_merge_kernel<HD>, pp, rows, G);
+}
+
 cudaError_t launch_extend_cascade(int head_dim, int G, const ExtendParams& p, const void* q, int batch,
                                   cudaStream_t st) {
   if (batch <= 0 || p.cas_prefix <= 0) return cudaSuccess;
-#define RX_EXT_CASE(HD_, G_) \
-  if (head_dim == HD_ && G == G_) return launch_extend_t<HD_, G_>(p, q, batch, batch, batch, st);
+  cudaError_t e = cudaSuccess;
+#define RX_EXT_CASE(HD_, G_)                                                            \
+  if (head_dim == HD_ && G == G_) {                                                     \
+    e = launch_extend_t<HD_, G_>(p, q, batch, batch, batch, st);                        \
+    if (e != cudaSuccess) return e;                                                     \
+    return launch_cascade_merge<HD_>(p, batch, G, st);                                  \
+  }
   RX_EXT_CASE(64, 1) RX_EXT_CASE(64, 2) RX_EXT_CASE(64, 4) RX_EXT_CASE(64, 8)
   RX_EXT_CASE(128, 1) RX_EXT_CASE(128, 2) RX_EXT_CASE(128, 4) RX_EXT_CASE(128, 8)
 #undef RX_EXT_CASE

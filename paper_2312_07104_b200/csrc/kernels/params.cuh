@@ -19,6 +19,18 @@ namespace rx {
 // different workspaces independent.
 constexpr size_t kWsHeader = 256;
 
+// Stream-K partition of the cascade work: W = units x tiles pair-tiles over
+// `ctas` virtual CTAs; virtual CTA c owns the pair-tiles [cut(c), cut(c+1)), cut(c) = c W / ctas,
+// split at unit boundaries into segments; a unit's segments are numbered by the virtual CTA that
+// owns them, from the CTA that holds its first tile.  Shared by the host plan and the kernel.
+__host__ __device__ inline int64_t cas_cut(int64_t c, int64_t W, int64_t ctas) { return c * W / ctas; }
+__host__ __device__ inline int cas_cta_of(int64_t x, int64_t W, int64_t ctas) {
+  return int(((x + 1) * ctas - 1) / W);     // the virtual CTA whose range holds pair-tile x
+}
+__host__ __device__ inline int cas_parts(int u, int tiles, int64_t W, int64_t ctas) {
+  return cas_cta_of(int64_t(u + 1) * tiles - 1, W, ctas) - cas_cta_of(int64_t(u) * tiles, W, ctas) + 1;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
 // per device context, so a process that drives several GPUs sets it on each.  Keyed by the kernel's
 // address (every instantiation of a kernel template has the same function TYPE).
@@ -79,9 +91,6 @@ struct DecodeParams {
   const int32_t* qo_indptr;
   const int32_t* prefix_lens;
   int col_tiles;
-  // merge: when > 0, every row has exactly this many partials (multi-query cascade:
-  // n_sh shared chunks + 1 suffix split) and seq_lens is not read
-  int fixed_splits;
 };
 
 struct ExtendParams {
@@ -101,24 +110,31 @@ struct ExtendParams {
   float scale_log2;
   int batch;                    // set by the launcher
   int max_qtiles;               // set by the launcher
-  // Cascade (shared-prefix) mode: the `batch` rows are decode queries of B requests
-  // that share cached prefix positions [0, prefix_lens[0]) (slots of table row
-  // rows[0]); no new tiles, no causal mask.  The prefix is cut into n_kv_splits
-  // chunks of kv_split_tiles tiles; each (q tile, kv head, chunk) item writes a
-  // normalized fp32 partial o and its log2-domain lse at split index
-  // part_base + chunk of the [B, h_q, part_splits] partial arrays.
+  // Cascade (shared-prefix) mode: the `batch` rows (decode queries, or every new token of a
+  // jump-forward step) share cached prefix positions [0, cas_prefix) (slots of table row rows[0]);
+  // no new tiles, no causal mask.  Work = units (q-tile pair, kv head), kv head major, x tiles of
+  // the prefix, partitioned stream-K over cas_ctas virtual CTAs (cas_cut above); each segment
+  // writes a normalized fp32 partial o and its log2-domain lse at part index `segment number` of
+  // the [batch, h_q, part_splits] partial arrays; the merge kernel that follows combines a row's
+  // cas_parts segment partials with its suffix partials at part indices n_sh .. n_sh + suffix
+  // splits (written by the kernel launched before the shared pass) into bf16 o.
   int cascade;
-  int kv_split_tiles;
-  int n_kv_splits;
+  int cas_ctas;
+  int cas_tiles;
+  int n_sh;                     // max segments of a unit = first suffix part index
   float* part_o;                // [B, h_q, part_splits, HD]
   float* part_lse;              // [B, h_q, part_splits]
   int part_splits;
-  int part_base;
   int cas_prefix;               // shared prefix length (cascade mode; prefix_lens unused)
-  // cascade partials launched as a programmatic dependent of the suffix decode: the grid may
-  // start before that decode completes (it reads only the shared prefix); its epilogue waits for
-  // the decode (hence the previous step's merge) before writing partials, and one thread per CTA
-  // waits before exiting, so the merge that waits on this grid also sees the decode's partials
+  // suffix partials per row: cas_fixed_suffix if > 0, else ceil((cas_seq_lens[row] - cas_kv_start)
+  // / cas_chunk) (the decode split plan)
+  int cas_fixed_suffix;
+  const int32_t* cas_seq_lens;
+  int cas_kv_start;
+  int cas_chunk;
+  // cascade launched as a programmatic dependent of the suffix decode: the grid may start before
+  // that decode completes (it reads only the shared prefix); its epilogue waits for the decode
+  // (hence the previous step, whose reads of the workspace are done) before writing partials
   int pdl;
   int* sched;                   // [2] work counters: the caller's workspace header (kWsHeader)
 };
@@ -150,25 +166,27 @@ inline size_t decode_ws_bytes(int h_q, int head_dim, int batch, int max_seq_len,
   return kWsHeader + n * head_dim * sizeof(float) + n * sizeof(float) + 256;
 }
 
-// Cascade plan (shared-prefix decode): the shared prefix [0, shared_len) is cut
-// into n_sh chunks of kv_split_tiles 128-token tiles so that (q tiles x kv heads
-// x chunks) gives ~2 items per SM of a 148-SM part (a constant, not the device's
-// count); the suffix [shared_len, seq_len) follows the ordinary split plan.
+// Cascade plan (shared-prefix decode / jump-forward extend): the shared prefix [0, shared_len) of
+// every (q-tile pair, kv head) unit is attended stream-K over `ctas` virtual CTAs (a constant
+// multiple of a 148-SM part, not the device's count, so TP shards reproduce on one GPU); the suffix
+// [shared_len, seq_len) follows the ordinary decode split plan.
 struct CascadePlan {
-  int n_sh;
-  int kv_split_tiles;
+  int n_sh;            // max segments of a unit (first suffix part index)
+  int ctas;
+  int tiles;
+  int units;
   DecodePlan suffix;
   int total_splits;
 };
 
-// Items per SM the shared-prefix split aims at (extend items are handed out dynamically, so more,
-// smaller items trade per-item overhead for a shorter tail).  RX_CASCADE_IPS overrides (A/B knob).
+// Virtual CTAs per SM of the shared-prefix pass (RX_CASCADE_IPS, A/B knob; 1 = one segment range
+// per SM of a 148-SM part, every SM busy for the same number of pair-tiles).
 inline int cascade_items_per_sm() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("RX_CASCADE_IPS");
-    v = e ? atoi(e) : 2;
-    if (v < 1 || v > 32) v = 2;
+    v = e ? atoi(e) : 1;
+    if (v < 1 || v > 32) v = 1;
   }
   return v;
 }
@@ -177,12 +195,18 @@ inline CascadePlan plan_cascade(int batch, int h_kv, int group, int max_seq_len,
   CascadePlan c{};
   const int tok = 128 / group;
   const int qt = (batch + tok - 1) / tok;
-  const int tiles = (shared_len + 127) / 128;
-  const int per_chunk = qt * h_kv;
-  int n = (cascade_items_per_sm() * 148 + per_chunk - 1) / per_chunk;
-  n = n < 1 ? 1 : (n > tiles ? tiles : n);
-  c.kv_split_tiles = (tiles + n - 1) / n;
-  c.n_sh = (tiles + c.kv_split_tiles - 1) / c.kv_split_tiles;
+  const int qp = (qt + 1) / 2;
+  c.units = qp * h_kv;
+  c.tiles = (shared_len + 127) / 128;
+  const int64_t W = int64_t(c.units) * c.tiles;
+  const int64_t want = int64_t(cascade_items_per_sm()) * 148;
+  const int64_t most = (W + 1) / 2;            // segments of >= 2 tiles: bounded partial counts
+  c.ctas = int(most < want ? most : want);
+  c.n_sh = 1;
+  for (int u = 0; u < c.units; ++u) {
+    const int n = cas_parts(u, c.tiles, W, c.ctas);
+    c.n_sh = n > c.n_sh ? n : c.n_sh;
+  }
   c.suffix = plan_decode(batch, h_kv, max_seq_len - shared_len);
   c.total_splits = c.n_sh + c.suffix.max_splits;
   return c;
@@ -199,7 +223,6 @@ cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, cons
 cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32_t* qo, const int32_t* ext,
                                 const int32_t* prefix, const int32_t* rows, const int32_t* rtt, int64_t rtt_stride,
                                 const void* k, const void* v, void* kpool, void* vpool, cudaStream_t st);
-cudaError_t launch_decode_merge(int head_dim, const DecodeParams& p, int batch, cudaStream_t st);
 int pdl_on();   // RX_PDL knob (decode.cu)
 cudaError_t launch_extend_cascade(int head_dim, int G, const ExtendParams& p, const void* q, int batch,
                                   cudaStream_t st);

@@ -168,6 +168,10 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* desc, uint
       "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// named barrier over `count` threads (ids 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
 // ---------------------------------------------------------------- register reallocation
 // Warpgroup-wide (all 4 warps of an aligned warpgroup execute it): move registers from the
 // producer warpgroup to the softmax warpgroups of a CTA.

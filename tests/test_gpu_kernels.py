@@ -443,7 +443,7 @@ def test_extend_cascade_vs_oracle(h_q, h_kv, hd, B, shared, max_pre_own, max_ext
                          torch.tensor(ext, dtype=torch.int32, device="cuda"), torch.from_numpy(indptr).cuda(), N,
                          max(ext), max(pre), shared, q.cuda(), kn.cuda(), vn.cuda(), kp, vp, o, ws)
     torch.cuda.synchronize()
-    assert rx.rx_last_launch_count() == 4                      # the cascade path ran
+    assert rx.rx_last_launch_count() == 4                      # the cascade path ran (store, suffix, shared, merge)
     pool = A.OraclePool(S, h_kv, hd)
     pool.store(np.arange(S), kpool.float().numpy(), vpool.float().numpy())
     ref = A.extend(pool, [rtt[b] for b in range(B)], pre, ext, q.float().numpy(), kn.float().numpy(),
