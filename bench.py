@@ -254,6 +254,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="tp", choices=["tp", "dp"],
+                    help="multi-GPU axis: tp = KV-head tensor parallelism (north star, default); dp = one "
+                         "data-parallel replica per GPU behind the router meta-tree (App. A.4), few-shot workload")
     ap.add_argument("--configs", default="C1,C2,C4,C5",
                     help="also time these workloads under the same protocol (reported under 'configs'); 'none'")
     args = ap.parse_args()
@@ -294,6 +297,9 @@ def main():
                 "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
+
+    if args.parallel == "dp":
+        return run_dp(args, world, rank, local)
 
     import torch
     import torch.distributed as dist
@@ -457,6 +463,98 @@ def main():
         }
         print(json.dumps(line))
     if tp_path:
+        dist.destroy_process_group()
+
+
+def run_dp(args, world, rank, local):
+    """Data-parallel replicas (App. A.4): one worker per GPU, each with
+    its own radix tree and pool, behind the router meta-tree.  Every rank replays the router and the
+    other workers' tree operations on the host (plan-only shadows: deterministic, so every rank holds
+    the same routing state with no communication) and runs its own worker's kernels; no data-path
+    collective.  Workload rxgen.workloads.dp_fewshot: one hint per subject prefix (the router spreads
+    them by load), then batches of interleaved few-shot questions the router sends to the worker that
+    caches their subject.  Weak scaling (subjects and requests grow with the worker count).  One step
+    = the whole workload from empty caches; value = tokens of ALL workers / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2312_07104_b200.dp import DPCluster
+    from paper_2312_07104_b200.engine import InputBank
+    from rxgen import workloads
+    from rxgen.workloads import Request
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    base = workloads.dp_fewshot(workers=world)
+    m = base.meta
+    pres = {}
+    for _, reqs in base.phases:
+        for r in reqs:
+            pres.setdefault(r.tag.split("s")[1].split("r")[0], r.prompt[:m["prefix"]])
+    hints = [Request(pres[str(s_)].copy(), 0, f"hint{s_}") for s_ in range(m["subjects"])]
+    wl = workloads.Workload("DP", base.shape, base.num_slots, base.vocab, base.seed,
+                            [("dp_batch", hints)] + list(base.phases), m)
+    lam = 0.1                   # affinity (1536 cached tokens) outweighs one batch's load imbalance
+    plan = DPCluster(wl, world, plan_only=True, load_weight=lam)
+    plan.run_workload()
+    bank = InputBank(plan.workers[rank].calls, wl.shape, plan.workers[rank].heads_q, plan.workers[rank].heads_kv, dev)
+    banks = [bank if w == rank else None for w in range(world)]
+    cl = DPCluster(wl, world, device=dev, local=rank, load_weight=lam)
+    flush = torch.empty(2 * torch.cuda.get_device_properties(dev).L2_cache_size, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        cl.reset()
+        cl.run_workload(banks)
+    torch.cuda.synchronize()
+    times, launches = [], 0
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            cl.reset()
+            cl.run_workload(banks)
+            b.record()
+            torch.cuda.synchronize()
+            barrier()
+            times.append(a.elapsed_time(b))
+            launches = cl.workers[rank].stats["launches"]
+    ms = sum(times)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = [e.stats for e in plan.workers]
+    tokens = sum(x["extend_tokens"] + x["decode_tokens"] for x in st)
+    prompt = sum(x["prompt_tokens"] for x in st)
+    cached = sum(x["cached_prompt_tokens"] for x in st)
+    # W-worker optimum: each subject prefix computed once in the whole cluster (hint), every
+    # question computed once, every later request hits its subject's prefix
+    optimum_computed = m["subjects"] * m["prefix"] + sum(len(r.prompt) - m["prefix"] for _, rq in base.phases
+                                                         for r in rq)
+    per_worker = [int(x["prompt_tokens"]) for x in st]
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": tokens * len(times) / (ms / 1000.0), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (rxgen dp_fewshot: per-subject few-shot prefixes, mock-model tokens)",
+            "config": {"workload": "DP few-shot (Llama-2-7B 32/32/128)", "parallelism": f"dp{world}",
+                       "subjects": m["subjects"], "prefix": m["prefix"], "tokens_per_step": tokens,
+                       "requests_per_step": sum(len(rq) for _, rq in wl.phases), "router_load_weight": lam,
+                       "l2_flush": "2x L2 write before each timed step"},
+            "cache_hit_rate": cached / prompt, "cache_hit_rate_optimal": 1.0 - optimum_computed / prompt,
+            "prompt_tokens_per_worker": per_worker, "gpu_launches": launches, "clocks": clk.summary(),
+            "e2e": None, "note": "e2e / cpu_baseline / configs: see the default (tp) bench line"}))
+    if world > 1:
         dist.destroy_process_group()
 
 

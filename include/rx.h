@@ -367,8 +367,11 @@ typedef struct {
  * k_pool[slots[i]] = k[i]; v_pool[slots[i]] = v[i] for i < n
  * (bit-exact copy).  If d_rtt_index is non-null, also rtt_flat[d_rtt_index[i]]
  * = slots[i] (d_rtt must then be non-null): the decode step's "append one
- * column to req_to_token" in the same launch.  Slots must be distinct and in
- * [1, num_slots).  Asynchronous on stream. */
+ * column to req_to_token" in the same launch.  d_k and d_v may both be null
+ * when d_rtt_index is given: then only the table entries are written (an
+ * output step whose K/V the following rx_extend stores itself, so no row is
+ * written twice).  Slots must be distinct and in [1, num_slots).
+ * Asynchronous on stream. */
 rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
                       const void* d_k, const void* d_v, void* d_k_pool, void* d_v_pool,
                       int64_t num_slots, int32_t* d_rtt, const int64_t* d_rtt_index,

@@ -365,7 +365,7 @@ def rx_store_kv(cfg: AttnCfg, slots, k, v, k_pool, v_pool, rtt=None, rtt_index=N
     n = slots.shape[0]
     st = lib.rx_store_kv(C.byref(cfg), n, _dev(slots, torch.int32, "slots"), _dev(k, torch.bfloat16, "k"),
                          _dev(v, torch.bfloat16, "v"), _dev(k_pool, torch.bfloat16, "k_pool"),
-                         _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0],
+                         _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0] if k_pool is not None else 1,
                          _dev(rtt, torch.int32, "rtt"), _dev(rtt_index, torch.int64, "rtt_index"), _stream(stream))
     _check(st, "rx_store_kv")
 

@@ -14,13 +14,17 @@
 //    O(n + words skipped) and free(k) O(k);
 //  * nodes: token/slot runs in std::vector<int32_t>, children in a hash map
 //    keyed by first token, id -> node map for handles;
-//  * evictable / cached token counts maintained incrementally.
+//  * evictable / cached token counts maintained incrementally, and so is the set of eviction
+//    candidates (non-root childless nodes with ref 0, ordered by (last_access, id), R2): every
+//    stamp, ref change, insert and eviction updates it, so evict(k) costs O(evicted leaves x log)
+//    instead of a walk over the whole tree.
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <new>
 #include <queue>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -101,6 +105,23 @@ struct rx_cache {
   int64_t evictable = 0;
   int64_t cached = 0;
   std::unordered_map<int64_t, Node*> by_id;
+  using CandKey = std::pair<std::pair<uint64_t, int64_t>, Node*>;
+  std::set<CandKey> cands;                 // eviction candidates, smallest (last_access, id) first
+
+  static CandKey key(Node* n) { return {{n->last_access, n->id}, n}; }
+  bool candidate(const Node* n) const { return n != &root && n->children.empty() && n->ref == 0; }
+  // every change of a node's stamp / ref / children goes through these two
+  void before_change(Node* n) {
+    if (candidate(n)) cands.erase(key(n));
+  }
+  void after_change(Node* n) {
+    if (candidate(n)) cands.insert(key(n));
+  }
+  void stamp(Node* n, uint64_t now) {
+    before_change(n);
+    n->last_access = now;
+    after_change(n);
+  }
 
   explicit rx_cache(int64_t n) : num_slots(n), free_slots(n) {
     for (int64_t s = 1; s < n; ++s) free_slots.set(s);
@@ -220,7 +241,7 @@ rx_status rx_match_prefix(rx_cache* c, const int32_t* tokens, int64_t n, rx_node
     Node* ch = it->second;
     size_t k = common_len(ch->tokens.data(), ch->tokens.size(), tokens + i, size_t(n - i));
     if (k < ch->tokens.size()) ch = c->split(ch, k);  // R3: eager split
-    ch->last_access = now;
+    c->stamp(ch, now);
     if (slots_out) std::memcpy(slots_out + i, ch->slots.data(), k * sizeof(int32_t));
     i += int64_t(k);
     cur = ch;
@@ -245,7 +266,7 @@ rx_status rx_insert(rx_cache* c, const int32_t* tokens, const int32_t* slots, in
     Node* ch = it->second;
     size_t k = common_len(ch->tokens.data(), ch->tokens.size(), tokens + i, size_t(n - i));
     if (k < ch->tokens.size()) ch = c->split(ch, k);
-    ch->last_access = now;
+    c->stamp(ch, now);
     if (std::memcmp(slots + i, ch->slots.data(), k * sizeof(int32_t)) != 0)   // R10 (usually equal)
       for (size_t j = 0; j < k; ++j)
         if (slots[i + j] != ch->slots[j]) dup.push_back(slots[i + j]);
@@ -261,7 +282,9 @@ rx_status rx_insert(rx_cache* c, const int32_t* tokens, const int32_t* slots, in
     leaf->parent = cur;
     leaf->ref = 0;
     leaf->last_access = now;
+    c->before_change(cur);                 // cur gains a child: no longer a candidate
     cur->children[tokens[i]] = leaf;
+    c->after_change(leaf);
     c->by_id[leaf->id] = leaf;
     c->evictable += added;
     c->cached += added;
@@ -279,6 +302,7 @@ rx_status rx_inc_ref(rx_cache* c, rx_node h, int64_t* d_evictable) {
   int64_t d = 0;
   for (; n != &c->root; n = n->parent) {
     if (n->ref == 0) d -= int64_t(n->tokens.size());
+    c->before_change(n);
     ++n->ref;
   }
   c->evictable += d;
@@ -293,8 +317,10 @@ rx_status rx_dec_ref(rx_cache* c, rx_node h, int64_t* d_evictable) {
   for (Node* m = n; m != &c->root; m = m->parent)
     if (m->ref < 1) return RX_E_UNDERFLOW;
   int64_t d = 0;
-  for (; n != &c->root; n = n->parent)
+  for (; n != &c->root; n = n->parent) {
     if (--n->ref == 0) d += int64_t(n->tokens.size());
+    c->after_change(n);
+  }
   c->evictable += d;
   if (d_evictable) *d_evictable = d;
   return RX_OK;
@@ -305,25 +331,12 @@ static rx_status evict_impl(rx_cache* c, int64_t needed, int64_t* evicted, rx_ev
   if (!c || !evicted) return RX_E_INVALID;
   *evicted = 0;
   if (needed <= 0) return RX_OK;
-  // candidates: non-root leaves with ref 0, min-ordered by (last_access, id) (R2)
-  using Key = std::pair<std::pair<uint64_t, int64_t>, Node*>;
-  auto cmp = [](const Key& a, const Key& b) { return a.first > b.first; };
-  std::priority_queue<Key, std::vector<Key>, decltype(cmp)> heap(cmp);
-  std::vector<Node*> stack;
-  for (auto& kv : c->root.children) stack.push_back(kv.second);
-  while (!stack.empty()) {
-    Node* n = stack.back();
-    stack.pop_back();
-    if (n->children.empty()) {
-      if (n->ref == 0) heap.push({{n->last_access, n->id}, n});
-    } else {
-      for (auto& kv : n->children) stack.push_back(kv.second);
-    }
-  }
   int64_t got = 0;
-  while (got < needed && !heap.empty()) {
-    Node* n = heap.top().second;
-    heap.pop();
+  // candidates: non-root leaves with ref 0, min-ordered by (last_access, id) (R2), kept
+  // incrementally in c->cands
+  while (got < needed && !c->cands.empty()) {
+    Node* n = c->cands.begin()->second;
+    c->cands.erase(c->cands.begin());
     Node* p = n->parent;
     p->children.erase(n->tokens[0]);
     int64_t len = int64_t(n->tokens.size());
@@ -344,7 +357,7 @@ static rx_status evict_impl(rx_cache* c, int64_t needed, int64_t* evicted, rx_ev
     c->cached -= len;
     c->by_id.erase(n->id);
     delete n;
-    if (p != &c->root && p->children.empty() && p->ref == 0) heap.push({{p->last_access, p->id}, p});
+    c->after_change(p);                    // a parent left childless with ref 0 becomes a candidate
   }
   *evicted = got;
   return RX_OK;

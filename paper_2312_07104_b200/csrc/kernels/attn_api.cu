@@ -61,7 +61,8 @@ rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
   rx_status s = check_cfg(cfg);
   if (s != RX_OK) return s;
   if (n < 0 || num_slots < 1) return RX_E_INVALID;
-  if (n > 0 && (!d_slots || !d_k || !d_v || !d_k_pool || !d_v_pool)) return RX_E_INVALID;
+  const bool table_only = !d_k && !d_v && d_rtt_index;      // append table entries only
+  if (n > 0 && (!d_slots || (!table_only && (!d_k || !d_v || !d_k_pool || !d_v_pool)))) return RX_E_INVALID;
   if (d_rtt_index && !d_rtt) return RX_E_INVALID;
   g_last_launches = 0;
   if (n == 0) return RX_OK;

@@ -25,8 +25,10 @@ __global__ void __launch_bounds__(256) store_kv_kernel(int64_t n, int row_vec, c
     const int64_t i = t / row_vec;
     const int c = int(t - i * row_vec);
     const int64_t slot = slots[i];
-    kpool[slot * row_vec + c] = k[t];
-    vpool[slot * row_vec + c] = v[t];
+    if (k) {                                       // null k / v: table append only
+      kpool[slot * row_vec + c] = k[t];
+      vpool[slot * row_vec + c] = v[t];
+    }
     if (rtt_idx && c == 0) rtt[rtt_idx[i]] = int32_t(slot);
   }
 }
@@ -75,7 +77,7 @@ cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32
 cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
                             void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  const int row_vec = row_bytes / 16;
+  const int row_vec = k ? row_bytes / 16 : 1;      // table only: one thread per row
   const int64_t total = n * row_vec;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;

@@ -25,14 +25,25 @@ def _common_prefix(seqs) -> int:
 
 
 class DPCluster:
-    def __init__(self, wl, workers: int, device="cuda", load_weight: float = 1.0, plan_only=False, record=False):
+    def __init__(self, wl, workers: int, device="cuda", load_weight: float = 1.0, plan_only=False, record=False,
+                 local=None):
+        """local=None: every worker runs (plan-only or on `device`, sequentially).  local=w: one
+        process per GPU — worker w runs its kernels here; the others are plan-only shadows that
+        replay their tree operations on the host, so every rank holds the same router state and
+        sees the same eviction reports without communication (the tree ops are deterministic, cf.
+        P:235)."""
         self.wl = wl
+        self.n = workers
+        self.local = local
         self.router = api.Router(workers)
         self.load_weight = load_weight
         self.loads = np.zeros(workers, dtype=np.int64)
         self.workers = []
         for w in range(workers):
-            e = Engine(wl, device=device, plan_only=plan_only, record=record)
+            shadow = plan_only or (local is not None and w != local)
+            e = Engine(wl, device=device, plan_only=shadow, record=record)
+            if local is not None and w != local:
+                e.collect_calls = False
             e.evict_listener = (lambda path, leaf_start, w=w: self.router.rx_router_queue_evict(w, path, leaf_start))
             self.workers.append(e)
         self.assignments = []
@@ -50,7 +61,7 @@ class DPCluster:
             idx = np.nonzero(wk == w)[0]
             if len(idx) == 0:
                 continue
-            if banks is not None:
+            if banks is not None and banks[w] is not None:
                 eng.bank = banks[w]
             sub = [reqs[i] for i in idx]
             # Frontend hint per worker ("the frontend sends the prefix first as a hint"):
@@ -72,6 +83,21 @@ class DPCluster:
         self.loads[:] = 0                      # the batch ran to completion
         self.router.rx_router_sync()
         return done
+
+    def reset(self):
+        """Fresh router, trees and pools for another pass (device pools and input banks are kept)."""
+        self.router = api.Router(self.n)
+        self.loads[:] = 0
+        self.assignments = []
+        self.batches = [[] for _ in range(self.n)]
+        for e in self.workers:
+            e.reset()
+
+    def run_workload(self, banks=None):
+        for kind, reqs in self.wl.phases:
+            assert kind == "dp_batch", kind
+            self.run_batch(reqs, banks)
+        return self
 
     def hit_rate(self):
         p = sum(e.stats["prompt_tokens"] for e in self.workers)

@@ -624,7 +624,8 @@ class Engine:
         ev0 = self._tbeg()
         nl0 = 0
         if incremental:
-            api.rx_store_kv(self.cfg, d_new, k_new, v_new, self.k_pool, self.v_pool, self._rtt, d_idx)
+            # table entries only: the rx_extend(_cascade) below stores the rows' K/V itself
+            api.rx_store_kv(self.cfg, d_new, None, None, None, None, self._rtt, d_idx)
             nl0 = api.rx_last_launch_count()
         if chunks is None and shared > 0:
             # every row shares cached positions [0, shared): attend them once for all rows (cascade)

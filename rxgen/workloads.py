@@ -161,6 +161,30 @@ def mix(seed: int = 0, groups: int = 4, per_group: int = 16, prefix: int = 1024,
                     {"groups": groups, "prefix": prefix})
 
 
+def dp_fewshot(seed: int = 0, workers: int = 1, subjects_per_worker: int = 2, prefix: int = 1536,
+               per_worker: int = 64, q_lo: int = 64, q_hi: int = 192, decode: int = 16, batches: int = 2,
+               num_slots: int = 32768) -> Workload:
+    """Data-parallel few-shot serving (App. A.4: "linear scaling and an optimal cache hit
+    rate" on MMLU with 4 workers): `workers` x subjects_per_worker unrelated 5-shot-like prefixes
+    (MMLU subjects), `batches` batches of per_worker x workers questions each, subject of request i =
+    i mod subjects (interleaved arrival), U[q_lo, q_hi] question tokens, `decode` output tokens.
+    Weak scaling: subjects and requests grow with the worker count.  Llama-2-7B attention shape
+    (32/32/128); num_slots per worker.  Phase kind "dp_batch" = one router dispatch."""
+    rng = np.random.default_rng(seed)
+    vocab = 32000
+    S = workers * subjects_per_worker
+    pres = [_rand_tokens(rng, prefix, vocab) for _ in range(S)]
+    phases = []
+    for b in range(batches):
+        reqs = []
+        for i in range(per_worker * workers):
+            q = _rand_tokens(rng, int(rng.integers(q_lo, q_hi + 1)), vocab)
+            reqs.append(Request(np.concatenate([pres[i % S], q]), decode, f"b{b}s{i % S}r{i}"))
+        phases.append(("dp_batch", reqs))
+    return Workload("DP", Shape(32, 32, 128), num_slots, vocab, seed, phases,
+                    {"workers": workers, "subjects": S, "prefix": prefix})
+
+
 # character-profile JSON schema (cf. the paper's JSON example P:106-108, P:259-261): long constant
 # keys (jump-forward edges) between short free fields
 JSON_REGEX = (r'\{"name": "[A-Z][a-z]{2,9}", "age": [1-9]\d?, "occupation": "(engineer|doctor|teacher|artist)", '

@@ -66,3 +66,51 @@ def test_dp_evictions_reach_router():
                 _, m, _ = e.cache.rx_match_prefix(path)
                 assert aff[w] <= m or aff[w] == len(path)
                 stack.append((c, path))
+
+
+def _dp_workload(W):
+    from rxgen.workloads import Request, Workload
+    base = workloads.dp_fewshot(workers=W, per_worker=16, q_lo=16, q_hi=48, decode=4)
+    m = base.meta
+    pres = {}
+    for _, reqs in base.phases:
+        for r in reqs:
+            pres.setdefault(int(r.tag.split("s")[1].split("r")[0]), r.prompt[:m["prefix"]])
+    hints = [Request(pres[s].copy(), 0, f"hint{s}") for s in range(m["subjects"])]
+    return base, Workload("DP", base.shape, base.num_slots, base.vocab, base.seed,
+                          [("dp_batch", hints)] + list(base.phases), m)
+
+
+def test_dp_weak_scaling_reaches_the_w_worker_optimum():
+    """bench.py --parallel dp's workload (App. A.4 P:638 "linear scaling and an optimal cache hit
+    rate"): with one hint per subject the router spreads the subjects over the workers by load, then
+    sends every question to the worker caching its subject — each prefix is computed once in the
+    whole cluster (the W-worker optimum) and per-worker prompt work is balanced for W = 1, 2, 4."""
+    for W in (1, 2, 4):
+        base, wl = _dp_workload(W)
+        cl = DPCluster(wl, W, plan_only=True, load_weight=0.1)
+        cl.run_workload()
+        st = [e.stats for e in cl.workers]
+        prompt = sum(x["prompt_tokens"] for x in st)
+        computed = prompt - sum(x["cached_prompt_tokens"] for x in st)
+        m = wl.meta
+        optimum = m["subjects"] * m["prefix"] + sum(len(r.prompt) - m["prefix"] for _, rq in base.phases for r in rq)
+        assert computed == optimum, (W, computed, optimum)
+        per = [x["prompt_tokens"] for x in st]
+        assert max(per) <= 1.05 * min(per), per
+
+
+def test_dp_local_shadows_replay_identical_trees():
+    """One process per GPU: the local worker runs for real while the others are plan-only shadows;
+    every shadow's trace equals that worker's trace in an all-plan cluster (deterministic replay, no
+    communication needed for routing)."""
+    _, wl = _dp_workload(3)
+    ref = DPCluster(wl, 3, plan_only=True, load_weight=0.1, record=True)
+    ref.run_workload()
+    for local in range(3):
+        cl = DPCluster(wl, 3, plan_only=True, load_weight=0.1, record=True, local=local)
+        cl.run_workload()
+        for w in range(3):
+            assert cl.workers[w].trace == ref.workers[w].trace
+        for a, b in zip(cl.assignments, ref.assignments):
+            assert np.array_equal(a[0], b[0])

@@ -64,6 +64,22 @@ def test_store_kv_bit_exact():
     assert kp[torch.from_numpy(untouched).cuda()].abs().sum().item() == 0
 
 
+def test_store_kv_table_only():
+    """rx_store_kv with null k / v and a table index (the engine's jump-forward output steps, whose
+    K/V the following rx_extend stores): only the table entries are written, the pools are not."""
+    rng = np.random.default_rng(1)
+    n = 50
+    cfg = rx.attn_cfg(8, 4, 128, 1 / math.sqrt(128))
+    slots = torch.from_numpy(rng.permutation(np.arange(1, 400))[:n].astype(np.int32)).cuda()
+    rtt = torch.zeros((4, 64), dtype=torch.int32, device="cuda")
+    idx = torch.from_numpy(rng.permutation(256)[:n].astype(np.int64)).cuda()
+    rx.rx_store_kv(cfg, slots, None, None, None, None, rtt, idx)
+    torch.cuda.synchronize()
+    assert rx.rx_last_launch_count() == 1
+    assert torch.equal(rtt.view(-1)[idx], slots)
+    assert int((rtt != 0).sum()) == n
+
+
 DEC_CASES = [
     # (h_q, h_kv, hd, seq_lens)
     (8, 2, 64, [1, 2, 15, 16, 17, 97, 300]),

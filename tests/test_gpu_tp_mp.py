@@ -1,0 +1,105 @@
+"""Tensor parallelism with REAL ranks (§3): two processes, each owning
+half of the KV heads (engine.shard_heads) with its own replicated radix tree and pool shard, run
+their kernels on the one GPU of this box and reassemble every attention call's output with an
+all-gather over a process group (gloo, through host copies: NCCL refuses two ranks on one device).
+Rank 0 compares the GATHERED outputs of every call with the fp64 oracle, every row, within the
+north-star tolerance, and both ranks' tree traces must be identical to the oracle's."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class _HostGather:
+    """gather(o_local [N, hq_local, hd] on cuda) -> [N, P, hq_local, hd] on cuda, via gloo."""
+
+    def __init__(self, dist):
+        self.dist = dist
+        self.world = dist.get_world_size()
+
+    def __call__(self, o_local):
+        torch.cuda.synchronize()
+        x = o_local.contiguous().cpu()
+        parts = [torch.empty_like(x) for _ in range(self.world)]
+        self.dist.all_gather(parts, x)
+        return torch.stack(parts, 0).to(o_local.device).permute(1, 0, 2, 3)
+
+
+def _worker(rank, world, port, wl_args, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2312_07104_b200.engine import Engine, plan_and_bank
+        from rxgen import workloads
+        wl = getattr(workloads, wl_args[0])(**wl_args[1])
+        _, bank = plan_and_bank(wl, "cuda", tp_rank=rank, tp_size=world)
+        e = Engine(wl, "cuda", tp_rank=rank, tp_size=world, record=True, keep_outputs=True,
+                   gather=_HostGather(dist))
+        e.run_workload(bank)
+        torch.cuda.synchronize()
+        outs = [(k, o.reshape(o.shape[0], -1, o.shape[-1]).float().cpu().numpy(), m) for k, o, m in e.outputs]
+        q.put((rank, e.trace, outs if rank == 0 else None, e.stats["launches"]))
+        dist.destroy_process_group()
+    except Exception as ex:  # surface errors to the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc() + repr(ex), 0))
+
+
+@pytest.mark.parametrize("wl_args", [
+    ("c5", dict(n_req=6, prefix=600, question=40, decode=5, num_slots=8192)),     # cascade decode path
+    ("c3", dict(sessions=4, turns=2, in_lo=30, in_hi=90, out_lo=4, out_hi=9, num_slots=8192)),
+])
+def test_tp2_processes_gathered_outputs_vs_oracle(wl_args):
+    from oracle.driver import OracleEngine
+    from rxgen import workloads
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, wl_args, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    res.sort(key=lambda r: r[0])
+    for r in res:
+        assert r[1] != "error", r[2]
+        assert r[3] > 0                                          # each rank launched its kernels
+    assert res[0][1] == res[1][1]                                # replicated trees
+    wl = getattr(workloads, wl_args[0])(**wl_args[1])
+    oe = OracleEngine(wl, materialize=True,
+                      sample_extend=lambda c, seqs: [(i, j) for i, s in enumerate(seqs)
+                                                     for j in range(s.n_prompt - s.prefix_len)],
+                      sample_decode=lambda c, st, run: list(range(len(run))))
+    oe.run_workload()
+    assert oe.trace == res[0][1]
+    outs = res[0][2]
+    ext = [x for x in outs if x[0] == "extend"]
+    dec = [x for x in outs if x[0] == "decode"]
+    errs = []
+    for key, ref in oe.outputs.items():
+        if key[0] == "extend":
+            _, call, bi, j = key
+            got = ext[call][1][int(np.sum(ext[call][2]["ext"][:bi])) + j]
+        else:
+            got = dec[key[1]][1][key[2]]
+        errs.append(np.abs(got.astype(np.float64) - ref).ravel())
+    err = np.concatenate(errs)
+    assert len(errs) > 100 and np.isfinite(err).all()
+    assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
