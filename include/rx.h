@@ -494,6 +494,37 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch,
 size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len,
                                          int32_t shared_len);
 
+/* ======================================================================= */
+/*  3. Tensor-parallel output all-gather over peer memory (A9)              */
+/* ======================================================================= */
+/* "For tensor parallelism, each GPU maintains a sharded KV cache. There is no
+ * need for additional synchronization because the tree operations are the
+ * same" (P:235 [§3]): a TP attention call's only exchange is reassembling its
+ * output head shards.  Each rank allocates ONE zero-filled device buffer of
+ * rx_tp_buffer_bytes(world, cap) bytes (cap = the largest shard in bytes, a
+ * multiple of 16), exports it with rx_tp_ipc_handle (RX_TP_HANDLE_BYTES
+ * opaque bytes), and maps every peer's buffer with rx_tp_ipc_open (on a
+ * multi-GPU node: NVLink / NVSwitch peer memory; ranks may also share one
+ * device).  rx_tp_allgather(d_src, bytes, peer_bufs, world, rank, cap, seq)
+ * then, in one kernel on the stream: stores this rank's shard d_src[0, bytes)
+ * into every rank's buffer (P2P stores), publishes seq to every rank, and
+ * waits for every rank's seq; when it completes the caller's own buffer holds
+ * the gathered output at offset 256 + (seq & 1)·world·cap, shard r at
+ * + r·cap.  peer_bufs: host array of world pointers (peer_bufs[rank] = the
+ * caller's own buffer).  Every rank must issue the same calls in the same
+ * order with seq = 1, 2, 3, ... (the gathered data of call seq stays valid
+ * until this rank issues call seq + 2).  world <= 8; bytes <= cap;
+ * RX_E_INVALID otherwise.  A rank that never calls leaves its peers waiting
+ * (like any collective) — for at most ~30 s, then the kernel traps (a launch
+ * error at the next synchronisation) instead of hanging the device. */
+#define RX_TP_HANDLE_BYTES 64
+size_t rx_tp_buffer_bytes(int32_t world, int64_t cap);
+rx_status rx_tp_ipc_handle(void* d_buf, void* handle_out);
+rx_status rx_tp_ipc_open(const void* handle, void** d_ptr);
+rx_status rx_tp_ipc_close(void* d_ptr);
+rx_status rx_tp_allgather(const void* d_src, int64_t bytes, void* const* peer_bufs, int32_t world, int32_t rank,
+                          int64_t cap, int64_t seq, void* stream);
+
 /* Number of kernel launches the last successful rx_extend / rx_decode /
  * rx_store_kv call on this thread issued (for launch accounting). */
 int32_t rx_last_launch_count(void);

@@ -92,6 +92,11 @@ SIGNATURES = {
                                            vp, vp, i64, vp, vp, sz, vp]),
     "rx_decode_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32, i32]),
     "rx_last_launch_count": (i32, []),
+    "rx_tp_buffer_bytes": (sz, [i32, i64]),
+    "rx_tp_ipc_handle": (C.c_int, [vp, vp]),
+    "rx_tp_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
+    "rx_tp_ipc_close": (C.c_int, [vp]),
+    "rx_tp_allgather": (C.c_int, [vp, i64, C.POINTER(vp), i32, i32, i64, i64, vp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

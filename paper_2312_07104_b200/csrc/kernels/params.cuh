@@ -54,6 +54,11 @@ inline int device_sms() {
   return v;
 }
 
+// TP peer-memory all-gather (tp.cu): buffer header = int64 flags [kTpMaxRanks] + an int32 CTA
+// counter, padded to kTpHeader bytes; two slots of world x cap bytes follow.
+constexpr int kTpMaxRanks = 8;
+constexpr int64_t kTpHeader = 256;
+
 struct DecodeParams {
   const __nv_bfloat16* q;       // [B, h_q, HD]
   const __nv_bfloat16* kpool;   // [S, h_kv, HD]

@@ -682,9 +682,15 @@ class Engine:
             flops = 4.0 * self.shape.head_dim * self.hq * float(np.sum(n * p_ + n * (n + 1) / 2))
             self._tend(ev0, "extend", flops, nl)
         if chunks is not None:
+            evg = self._tbeg()
             o = self.gather.finish(handles, out)
+            if evg is not None:
+                self._tend(evg, "gather", 0.0, 0)
         elif self.gather is not None:
+            evg = self._tbeg()
             o = self.gather(o)
+            if evg is not None:
+                self._tend(evg, "gather", 0.0, 0)
         if self.sink is not None:
             self.sink("extend", o)
         if self.keep_outputs:
@@ -767,7 +773,10 @@ class Engine:
                 works.append(w)
             nl_run += nl
             if self.gather is not None:
+                evg = self._tbeg()
                 o = self.gather(o)
+                if evg is not None:
+                    self._tend(evg, "gather", 0.0, 0)
             if self.sink is not None:
                 self.sink("decode", o)
             if self.keep_outputs:

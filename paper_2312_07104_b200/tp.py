@@ -9,9 +9,11 @@ same."  So:
   hash of the tree to prove it);
 * rank r owns q heads [r*H_q/P, (r+1)*H_q/P) and the kv heads they read, i.e.
   its slice of the pool (``engine.shard_heads``);
-* the only exchange is ONE all_gather of the bf16 attention output per call,
-  over NCCL on NVLink (torch.distributed), returned as a strided view — no
-  permute copy.
+* the only exchange is ONE all-gather of the bf16 attention output per call:
+  ``P2PGather`` (librx rx_tp_allgather: one kernel stores the shard into every
+  peer's IPC-mapped buffer over NVLink and synchronises with flags — no NCCL
+  launch per call) for calls up to its capacity, NCCL ``all_gather_into_tensor``
+  (``Gather``) for larger ones and for the chunked, overlapped extend gathers.
 """
 from __future__ import annotations
 
@@ -63,7 +65,88 @@ class Gather:
         return out.permute(1, 0, 2, 3)
 
 
-def make_gather(group=None):
+class P2PGather:
+    """gather(o_local) over peer memory (include/rx.h section 3): every rank holds one zero-filled
+    IPC buffer of rx_tp_buffer_bytes(world, cap); handles are exchanged once through the process
+    group; each call is one rx_tp_allgather kernel on the current stream plus one device copy of the
+    gathered [P, bytes] slot into a fresh tensor (so the result outlives the two-slot ring).  Calls
+    whose shard exceeds `cap` bytes, and the chunked extend gathers (alloc / start / finish), go
+    through NCCL (``Gather``)."""
+
+    def __init__(self, cap_bytes=8 << 20, group=None, device=None):
+        import ctypes as C
+        from ._lib import lib
+        self._lib, self._C = lib, C
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cap = (int(cap_bytes) + 15) // 16 * 16
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.buf = torch.zeros(int(lib.rx_tp_buffer_bytes(self.world, self.cap)), dtype=torch.uint8, device=dev)
+        h = (C.c_uint8 * 64)()
+        st = lib.rx_tp_ipc_handle(C.c_void_p(self.buf.data_ptr()), C.cast(h, C.c_void_p))
+        if st != 0:
+            raise RuntimeError(f"rx_tp_ipc_handle: {st}")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self._opened = []
+        ptrs = []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(self.buf.data_ptr())
+                continue
+            p = C.c_void_p()
+            hh = (C.c_uint8 * 64).from_buffer_copy(hb)
+            st = lib.rx_tp_ipc_open(C.cast(hh, C.c_void_p), C.byref(p))
+            if st != 0:
+                raise RuntimeError(f"rx_tp_ipc_open(rank {r}): {st}")
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self.peers = (C.c_void_p * self.world)(*ptrs)
+        self.seq = 0
+        self.fallback = Gather(group)
+        dist.barrier(group=group)              # every rank mapped every buffer before the first call
+
+    def __call__(self, o_local: torch.Tensor) -> torch.Tensor:
+        o_local = o_local.contiguous()
+        n = o_local.numel() * o_local.element_size()
+        if n > self.cap or n % 16:
+            return self.fallback(o_local)
+        self.seq += 1
+        C = self._C
+        st = self._lib.rx_tp_allgather(C.c_void_p(o_local.data_ptr()), n, self.peers, self.world, self.rank,
+                                       self.cap, self.seq, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if st != 0:
+            raise RuntimeError(f"rx_tp_allgather: {st}")
+        base = 256 + (self.seq & 1) * self.world * self.cap
+        slot = self.buf[base:base + self.world * self.cap].view(self.world, self.cap)[:, :n]
+        out = torch.empty((self.world,) + tuple(o_local.shape), dtype=o_local.dtype, device=o_local.device)
+        out.view(self.world, -1).view(torch.uint8).copy_(slot)
+        return out.permute(1, 0, 2, 3)
+
+    # chunked, overlapped extend gathers: NCCL
+    def alloc(self, n, hq_local, hd, dtype, device):
+        return self.fallback.alloc(n, hq_local, hd, dtype, device)
+
+    def start(self, o_part, out, r0, r1):
+        return self.fallback.start(o_part, out, r0, r1)
+
+    @staticmethod
+    def finish(handles, out):
+        return Gather.finish(handles, out)
+
+    def close(self):
+        for p in self._opened:
+            self._lib.rx_tp_ipc_close(p)
+        self._opened = []
+
+
+def make_gather(group=None, p2p=True):
+    """The TP output gather: peer-memory (P2PGather) on a CUDA (NCCL) group unless p2p=False or
+    RX_TP_NCCL=1; the plain collective (Gather) otherwise (e.g. gloo groups in CPU tests)."""
+    import os
+    if p2p and dist.get_backend(group) == "nccl" and os.environ.get("RX_TP_NCCL", "0") != "1":
+        return P2PGather(group=group)
     return Gather(group)
 
 

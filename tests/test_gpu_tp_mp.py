@@ -38,7 +38,7 @@ class _HostGather:
         return torch.stack(parts, 0).to(o_local.device).permute(1, 0, 2, 3)
 
 
-def _worker(rank, world, port, wl_args, q):
+def _worker(rank, world, port, wl_args, q, kind="host"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -49,8 +49,12 @@ def _worker(rank, world, port, wl_args, q):
         from rxgen import workloads
         wl = getattr(workloads, wl_args[0])(**wl_args[1])
         _, bank = plan_and_bank(wl, "cuda", tp_rank=rank, tp_size=world)
-        e = Engine(wl, "cuda", tp_rank=rank, tp_size=world, record=True, keep_outputs=True,
-                   gather=_HostGather(dist))
+        if kind == "p2p":
+            from paper_2312_07104_b200.tp import P2PGather
+            gather = P2PGather(cap_bytes=4 << 20)
+        else:
+            gather = _HostGather(dist)
+        e = Engine(wl, "cuda", tp_rank=rank, tp_size=world, record=True, keep_outputs=True, gather=gather)
         e.run_workload(bank)
         torch.cuda.synchronize()
         outs = [(k, o.reshape(o.shape[0], -1, o.shape[-1]).float().cpu().numpy(), m) for k, o, m in e.outputs]
@@ -61,17 +65,20 @@ def _worker(rank, world, port, wl_args, q):
         q.put((rank, "error", traceback.format_exc() + repr(ex), 0))
 
 
+@pytest.mark.parametrize("kind", ["host", "p2p"])
 @pytest.mark.parametrize("wl_args", [
     ("c5", dict(n_req=6, prefix=600, question=40, decode=5, num_slots=8192)),     # cascade decode path
     ("c3", dict(sessions=4, turns=2, in_lo=30, in_hi=90, out_lo=4, out_hi=9, num_slots=8192)),
 ])
-def test_tp2_processes_gathered_outputs_vs_oracle(wl_args):
+def test_tp2_processes_gathered_outputs_vs_oracle(wl_args, kind):
+    """kind = host: gloo all-gather through host copies; p2p: librx rx_tp_allgather (each rank's
+    kernel stores its shard into the peer's IPC-mapped buffer and synchronises by flags)."""
     from oracle.driver import OracleEngine
     from rxgen import workloads
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, wl_args, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, wl_args, q, kind), daemon=True) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(2)]
@@ -103,3 +110,49 @@ def test_tp2_processes_gathered_outputs_vs_oracle(wl_args):
     err = np.concatenate(errs)
     assert len(errs) > 100 and np.isfinite(err).all()
     assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
+
+
+def _p2p_worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2312_07104_b200.tp import P2PGather
+        g = P2PGather(cap_bytes=1 << 20)
+        ok = True
+        for call, n in enumerate([1, 7, 64, 255, 2048, 1, 4096, 33]):
+            o = torch.full((n, 4, 128), float(rank * 1000 + call), dtype=torch.bfloat16, device="cuda")
+            o[:, :, 0] = torch.arange(n, dtype=torch.float32).to(torch.bfloat16).cuda()[:, None]
+            full = g(o)                                           # [n, P, 4, 128]
+            torch.cuda.synchronize()
+            for r in range(world):
+                exp = torch.full((n, 4, 127), float(r * 1000 + call), dtype=torch.bfloat16, device="cuda")
+                ok &= torch.equal(full[:, r, :, 1:], exp)
+                ok &= torch.equal(full[:, r, :, 0], torch.arange(n, dtype=torch.float32).to(torch.bfloat16)
+                                  .cuda()[:, None].expand(n, 4))
+        q.put((rank, bool(ok), g.seq))
+        g.close()
+        dist.destroy_process_group()
+    except Exception as ex:
+        import traceback
+        q.put((rank, "error", traceback.format_exc() + repr(ex)))
+
+
+def test_p2p_allgather_two_ranks_bitwise():
+    """rx_tp_allgather between two processes (IPC-mapped buffers, flag synchronisation; here both
+    ranks share one device): eight back-to-back calls of different sizes (both slots of the ring,
+    odd sizes) reassemble every rank's shard bit for bit in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, 2, port, q), daemon=True) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[1] != "error", r[2]
+        assert r[1] is True and r[2] == 8, r
