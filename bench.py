@@ -353,12 +353,17 @@ def main():
         peak = peaks["hbm_gbs"]
         roof = {"bound": "hbm", "unit": "GB/s", "kernel": f"rx_{kind}"}
     # traffic: DRAM bytes per launch from the committed `ncu --set full` capture of this kernel in
-    # this workload (profiles/r1_ncu_<kind>_traffic_<wl>.json, scripts/ncu_traffic.py), expressed for
+    # this workload (profiles/r<k>_ncu_<kind>_traffic_<wl>.json, scripts/ncu_traffic.py), expressed for
     # this run's average launch: (captured DRAM bytes / captured algorithmic bytes) x algorithmic
     # bytes per launch here
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", f"r1_ncu_{kind}_traffic_{wl.name}.json")
-    if os.path.exists(tp):
+    tp = None
+    for rnd in ("r2", "r1"):                          # the newest committed capture
+        cand = os.path.join(ROOT, "profiles", f"{rnd}_ncu_{kind}_traffic_{wl.name}.json")
+        if os.path.exists(cand):
+            tp = cand
+            break
+    if tp is not None:
         with open(tp) as f:
             tj = json.load(f)
         traffic = tj["traffic_over_algorithmic"] * (kwork / kcalls)

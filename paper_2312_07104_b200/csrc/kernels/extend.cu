@@ -785,27 +785,36 @@ __global__ void __launch_bounds__(kCasMergeWarps * 32) cascade_merge_kernel(cons
   const int nk = parts + ns;
   const int64_t base = pair * p.part_splits;
   auto idx = [&](int k) { return k < parts ? k : p.n_sh + (k - parts); };
+  // lane k holds partial k's lse (32 at a time): one load instruction for every lse of the row, the
+  // weights by warp reductions, then the partials' float4s with up to 8 loads in flight per lane
+  constexpr int V = HD / 32;                       // 4 (hd 128) or 2 (hd 64) floats per lane
   float M = -INFINITY;
-  for (int k = lane; k < nk; k += 32) M = fmaxf(M, p.part_lse[base + idx(k)]);
+  for (int k0 = 0; k0 < nk; k0 += 32)
+    M = fmaxf(M, k0 + lane < nk ? p.part_lse[base + idx(k0 + lane)] : -INFINITY);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  constexpr int V = HD / 32;                       // 4 (hd 128) or 2 (hd 64) floats per lane
   float acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   float W = 0.f;
-#pragma unroll 4
-  for (int k = 0; k < nk; ++k) {
-    const int64_t pr = base + idx(k);
-    const float w = fast_exp2(p.part_lse[pr] - M);
-    W += w;
-    const float* src = p.part_o + pr * HD + lane * V;
-    if constexpr (V == 4) {
-      const float4 x = *reinterpret_cast<const float4*>(src);
-      acc[0] += w * x.x, acc[1] += w * x.y, acc[2] += w * x.z, acc[3] += w * x.w;
-    } else {
-      const float2 x = *reinterpret_cast<const float2*>(src);
-      acc[0] += w * x.x, acc[1] += w * x.y;
+  for (int k0 = 0; k0 < nk; k0 += 32) {
+    const float wl = k0 + lane < nk ? fast_exp2(p.part_lse[base + idx(k0 + lane)] - M) : 0.f;
+    float ws = wl;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+    W += ws;
+    const int n = min(32, nk - k0);
+#pragma unroll 8
+    for (int k = 0; k < n; ++k) {
+      const float w = __shfl_sync(0xffffffffu, wl, k);
+      const float* src = p.part_o + (base + idx(k0 + k)) * HD + lane * V;
+      if constexpr (V == 4) {
+        const float4 x = *reinterpret_cast<const float4*>(src);
+        acc[0] += w * x.x, acc[1] += w * x.y, acc[2] += w * x.z, acc[3] += w * x.w;
+      } else {
+        const float2 x = *reinterpret_cast<const float2*>(src);
+        acc[0] += w * x.x, acc[1] += w * x.y;
+      }
     }
   }
   const float inv = 1.f / W;
