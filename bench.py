@@ -110,9 +110,9 @@ def _oracle_session(args):
             return r
 
         def _attend(self, seq, p):
-            t = time.perf_counter()
+            t, t_in = time.perf_counter(), self.t_input
             r = super()._attend(seq, p)
-            self.t_att[self.phase] += time.perf_counter() - t
+            self.t_att[self.phase] += time.perf_counter() - t - (self.t_input - t_in)   # q generation excluded
             return r
 
     cnt = {"ext": 0, "ext_s": 0, "dec": 0, "dec_s": 0}

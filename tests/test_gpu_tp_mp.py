@@ -123,7 +123,7 @@ def _p2p_worker(rank, world, port, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         from paper_2312_07104_b200.tp import P2PGather
-        g = P2PGather(cap_bytes=1 << 20)
+        g = P2PGather(cap_bytes=4 << 20)          # every call below fits: all 8 go through rx_tp_allgather
         ok = True
         for call, n in enumerate([1, 7, 64, 255, 2048, 1, 4096, 33]):
             o = torch.full((n, 4, 128), float(rank * 1000 + call), dtype=torch.bfloat16, device="cuda")
