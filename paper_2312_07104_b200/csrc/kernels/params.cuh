@@ -207,6 +207,16 @@ inline CascadePlan plan_cascade(int batch, int h_kv, int group, int max_seq_len,
   const int64_t want = int64_t(cascade_items_per_sm()) * 148;
   const int64_t most = (W + 1) / 2;            // segments of >= 2 tiles: bounded partial counts
   c.ctas = int(most < want ? most : want);
+  static int align = -1;                       // RX_CASCADE_ALIGN=1 (A/B knob): whole units per CTA
+  if (align < 0) {
+    const char* e = getenv("RX_CASCADE_ALIGN");
+    align = e ? atoi(e) : 0;
+  }
+  if (align && c.units <= want) {
+    const int per = int(want / c.units);       // CTAs per unit: every CTA one segment of one unit
+    const int k = per < c.tiles ? per : c.tiles;
+    c.ctas = c.units * (k > 0 ? k : 1);
+  }
   c.n_sh = 1;
   for (int u = 0; u < c.units; ++u) {
     const int n = cas_parts(u, c.tiles, W, c.ctas);
