@@ -207,13 +207,16 @@ inline CascadePlan plan_cascade(int batch, int h_kv, int group, int max_seq_len,
   const int64_t want = int64_t(cascade_items_per_sm()) * 148;
   const int64_t most = (W + 1) / 2;            // segments of >= 2 tiles: bounded partial counts
   c.ctas = int(most < want ? most : want);
-  static int align = -1;                       // RX_CASCADE_ALIGN=1 (A/B knob): whole units per CTA
+  // When the units fit the SMs, every CTA gets ONE segment of one unit (ctas = units x k): a
+  // second segment per CTA costs another pipeline fill and partial write (C5 step 93 -> 81 us,
+  // profiles/r2_kbench_cascade_aligned.txt); RX_CASCADE_ALIGN=0 keeps the plain stream-K cut.
+  static int align = -1;
   if (align < 0) {
     const char* e = getenv("RX_CASCADE_ALIGN");
-    align = e ? atoi(e) : 0;
+    align = e ? atoi(e) : 1;
   }
   if (align && c.units <= want) {
-    const int per = int(want / c.units);       // CTAs per unit: every CTA one segment of one unit
+    const int per = int(want / c.units);
     const int k = per < c.tiles ? per : c.tiles;
     c.ctas = c.units * (k > 0 ? k : 1);
   }
