@@ -13,8 +13,15 @@ from __future__ import annotations
 import torch
 
 
+def _aligned(nb):
+    return (nb + 255) // 256 * 256
+
+
 class _Prefetcher:
-    """Indexable like a list of (q, k, v) device tensors; element i is copied ahead of use."""
+    """Indexable like a list of (q, k, v) device tensors; element i is copied ahead of use into a
+    preallocated device ring of depth + 1 slots (no allocation per call: a caching-allocator miss
+    on a ~1 GB extend input can stall the host behind the device).  Slot reuse waits on an event
+    recorded on the compute stream once the previous call that used the slot was enqueued."""
 
     def __init__(self, host_list, device, depth, stream):
         self.lst = host_list
@@ -23,6 +30,10 @@ class _Prefetcher:
         self.stream = stream
         self.pending = {}
         self.h2d_bytes = sum(t.numel() * t.element_size() for tr in host_list for t in tr)
+        cap = max([sum(_aligned(t.numel() * t.element_size()) for t in tr) for tr in host_list] or [256])
+        self.nslots = depth + 1
+        self.ring = [torch.empty(cap, dtype=torch.uint8, device=device) for _ in range(self.nslots)]
+        self.free = [None] * self.nslots
 
     def reset(self):
         self.pending.clear()
@@ -30,27 +41,41 @@ class _Prefetcher:
     def _issue(self, i):
         if i >= len(self.lst) or i in self.pending:
             return
+        slot = i % self.nslots
+        buf = self.ring[slot]
         with torch.cuda.stream(self.stream):
-            ts = tuple(t.to(self.dev, non_blocking=True) for t in self.lst[i])
+            if self.free[slot] is not None:
+                self.stream.wait_event(self.free[slot])
+            views, off = [], 0
+            for t in self.lst[i]:
+                nb = t.numel() * t.element_size()
+                v = buf[off:off + nb].view(t.dtype).view(t.shape)
+                v.copy_(t, non_blocking=True)
+                views.append(v)
+                off += _aligned(nb)
             ev = torch.cuda.Event()
             ev.record(self.stream)
-        self.pending[i] = (ts, ev)
+        self.pending[i] = (tuple(views), ev)
 
     def __getitem__(self, i):
+        cur = torch.cuda.current_stream()
+        if i > 0:
+            # call i - 1 is fully enqueued: its slot is free once the compute stream gets here
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self.free[(i - 1) % self.nslots] = ev
         for j in range(i, i + self.depth):
             self._issue(j)
         ts, ev = self.pending.pop(i)
-        cur = torch.cuda.current_stream()
         cur.wait_event(ev)
-        for t in ts:
-            t.record_stream(cur)           # the allocator must not recycle them before `cur` is done
         return ts
 
 
 class _BlockPrefetcher:
     """Like _Prefetcher for many small calls (decode steps): the calls' tensors live back to back in
-    ONE pinned byte buffer and are copied `block` calls per cudaMemcpy, `depth` blocks ahead, so
-    the host issues one copy per block instead of three per call."""
+    ONE pinned byte buffer and are copied `block` calls per cudaMemcpy, `depth` blocks ahead, into a
+    device ring of depth + 1 block buffers, so the host issues one copy per block instead of three
+    per call and nothing is allocated per block."""
 
     def __init__(self, host_list, device, block, depth, stream):
         self.dev, self.block, self.depth, self.stream = device, block, depth, stream
@@ -61,7 +86,7 @@ class _BlockPrefetcher:
             for t in tr:
                 nb = t.numel() * t.element_size()
                 m.append((off, nb, t.dtype, tuple(t.shape)))
-                off += (nb + 255) // 256 * 256
+                off += _aligned(nb)
             self.meta.append(m)
         self.h2d_bytes = sum(t.numel() * t.element_size() for tr in host_list for t in tr)
         self.buf = torch.empty(max(off, 1), dtype=torch.uint8, pin_memory=True)
@@ -75,6 +100,10 @@ class _BlockPrefetcher:
             first = self.meta[b0][0][0]
             last = self.meta[b1 - 1][-1]
             self.ranges.append((first, last[0] + last[1]))
+        cap = max([b - a for a, b in self.ranges] or [256])
+        self.nslots = depth + 1
+        self.ring = [torch.empty(cap, dtype=torch.uint8, device=device) for _ in range(self.nslots)]
+        self.free = [None] * self.nslots
         self.pending = {}
 
     def reset(self):
@@ -84,21 +113,29 @@ class _BlockPrefetcher:
         if j >= len(self.ranges) or j in self.pending:
             return
         a, b = self.ranges[j]
+        slot = j % self.nslots
         with torch.cuda.stream(self.stream):
-            d = self.buf[a:b].to(self.dev, non_blocking=True)
+            if self.free[slot] is not None:
+                self.stream.wait_event(self.free[slot])
+            d = self.ring[slot][:b - a]
+            d.copy_(self.buf[a:b], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.stream)
         self.pending[j] = (d, ev, a, False)
 
     def __getitem__(self, i):
         j = i // self.block
+        cur = torch.cuda.current_stream()
+        if i % self.block == 0 and j > 0:
+            # every call of block j - 1 is enqueued: its slot is free once the compute stream gets here
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self.free[(j - 1) % self.nslots] = ev
         for k in range(j, j + self.depth):
             self._issue(k)
         d, ev, a, waited = self.pending[j]
-        cur = torch.cuda.current_stream()
         if not waited:
             cur.wait_event(ev)
-            d.record_stream(cur)
             self.pending[j] = (d, ev, a, True)
         out = tuple(d[o - a:o - a + nb].view(dt).view(shape) for o, nb, dt, shape in self.meta[i])
         if i % self.block == self.block - 1 or i == len(self.meta) - 1:

@@ -28,7 +28,11 @@ def main():
             hb.ext._issue(i)
         for j in range(len(hb.dec.ranges)):
             hb.dec._issue(j)
+    import types
+    ext_only = types.SimpleNamespace(ext=hb.ext, dec=bank.dec)      # extend inputs via H2D only
+    dec_only = types.SimpleNamespace(ext=bank.ext, dec=hb.dec)      # decode inputs via H2D only
     for name, inputs, sk in (("device", bank, None), ("copy||", bank, None), ("h2d", hb, None),
+                             ("h2d-ext", ext_only, None), ("h2d-dec", dec_only, None),
                              ("d2h", bank, sink), ("both", hb, sink)):
         eng.sink = sk
         ts = []
@@ -38,7 +42,7 @@ def main():
             a, b = torch.cuda.Event(True), torch.cuda.Event(True)
             sink.reset()
             a.record()
-            if inputs is hb or name == "copy||":
+            if inputs is not bank:
                 hb.reset()
             if name == "copy||":
                 all_copies()
