@@ -377,6 +377,14 @@ rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
                       int64_t num_slots, int32_t* d_rtt, const int64_t* d_rtt_index,
                       void* stream);
 
+/* Host -> device copy of small per-call metadata by the SMs (one kernel on
+ * stream): h_src must be pinned host memory (cudaHostAlloc / a pinned torch
+ * tensor; RX_E_INVALID otherwise), read over PCIe through its device mapping.
+ * Unlike cudaMemcpyAsync it does not queue on the copy engines, where a large
+ * input prefetch on another stream would hold it (engines serve copies in
+ * submission order).  The host buffer must stay valid until the kernel ran. */
+rx_status rx_copy_h2d(void* d_dst, const void* h_src, int64_t bytes, void* stream);
+
 /* Extend (prefill with prefix reuse) for a ragged batch.
  * Request b has prefix_len[b] cached tokens (slots rtt[row_b][0..prefix_len))
  * and extend_len[b] >= 0 new tokens at positions prefix_len .. prefix_len +

@@ -8,7 +8,7 @@ harness that drives it.  It never imports ``oracle/``.
 from .api import (RadixCache, Fsm, attn_cfg, rx_store_kv, rx_extend, rx_decode, rx_decode_append, rx_decode_cascade_append,
                   rx_decode_cascade_workspace_bytes, rx_extend_workspace_bytes, rx_extend_cascade,
                   rx_extend_cascade_workspace_bytes,
-                  rx_decode_workspace_bytes, rx_last_launch_count)
+                  rx_decode_workspace_bytes, rx_last_launch_count, rx_copy_h2d)
 from ._lib import RxError, LIB_PATH
 
 __all__ = ["RadixCache", "Fsm", "attn_cfg", "rx_store_kv", "rx_extend", "rx_decode", "rx_decode_append", "rx_decode_cascade_append",

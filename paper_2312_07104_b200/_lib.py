@@ -92,6 +92,7 @@ SIGNATURES = {
                                            vp, vp, i64, vp, vp, sz, vp]),
     "rx_decode_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32, i32]),
     "rx_last_launch_count": (i32, []),
+    "rx_copy_h2d": (C.c_int, [vp, vp, i64, vp]),
     "rx_tp_buffer_bytes": (sz, [i32, i64]),
     "rx_tp_ipc_handle": (C.c_int, [vp, vp]),
     "rx_tp_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),

@@ -471,5 +471,17 @@ def rx_decode_cascade_append(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int
     _check(st, "rx_decode_cascade_append")
 
 
+def rx_copy_h2d(dst, src_pinned, stream=None):
+    """dst (CUDA tensor) <- src_pinned (pinned CPU tensor, same byte size), copied by an SM kernel."""
+    import torch
+    if not src_pinned.is_pinned():
+        raise ValueError("rx_copy_h2d: the source must be pinned host memory")
+    nb = src_pinned.numel() * src_pinned.element_size()
+    if dst.numel() * dst.element_size() != nb:
+        raise ValueError("rx_copy_h2d: size mismatch")
+    _check(lib.rx_copy_h2d(_dev(dst, None, "dst"), C.c_void_p(src_pinned.data_ptr()), nb, _stream(stream)),
+           "rx_copy_h2d")
+
+
 def rx_last_launch_count() -> int:
     return lib.rx_last_launch_count()

@@ -73,6 +73,19 @@ rx_status rx_store_kv(const rx_attn_cfg* cfg, int64_t n, const int32_t* d_slots,
   return RX_OK;
 }
 
+rx_status rx_copy_h2d(void* d_dst, const void* h_src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!d_dst || !h_src))) return RX_E_INVALID;
+  g_last_launches = 0;
+  if (bytes == 0) return RX_OK;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h_src) != cudaSuccess || a.type != cudaMemoryTypeHost) return RX_E_INVALID;
+  if (rx::launch_copy_h2d(d_dst, a.devicePointer ? a.devicePointer : h_src, bytes,
+                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return RX_E_CUDA;
+  g_last_launches = 1;
+  return RX_OK;
+}
+
 size_t rx_decode_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len) {
   if (check_cfg(cfg) != RX_OK || batch <= 0 || max_seq_len <= 0) return 0;
   return rx::decode_ws_bytes(cfg->h_q, cfg->head_dim, batch, max_seq_len, cfg->h_kv);

@@ -236,6 +236,7 @@ inline size_t cascade_ws_bytes(int h_q, int head_dim, int batch, int h_kv, int m
   return kWsHeader + n * head_dim * sizeof(float) + n * sizeof(float) + 256;
 }
 
+cudaError_t launch_copy_h2d(void* dst, const void* src, int64_t bytes, cudaStream_t st);
 cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, const void* k, const void* v,
                             void* kpool, void* vpool, int32_t* rtt, const int64_t* rtt_idx, cudaStream_t st);
 cudaError_t launch_extend_store(int64_t n, int batch, int row_bytes, const int32_t* qo, const int32_t* ext,

@@ -87,4 +87,27 @@ cudaError_t launch_store_kv(int64_t n, int row_bytes, const int32_t* slots, cons
   return cudaPeekAtLastError();
 }
 
+// Host -> device copy of small metadata (slot tables, decode step records) by the SMs: the kernel
+// reads pinned (UVA-mapped) host memory over PCIe itself, so the upload does not queue on the copy
+// engines behind a large input prefetch of another stream (copy-engine work is served in
+// submission order).  16-byte vectors when both pointers allow, bytes otherwise.
+__global__ void __launch_bounds__(256) copy_h2d_kernel(char* __restrict__ dst, const char* __restrict__ src,
+                                                       int64_t bytes) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  const int64_t nv = vec ? bytes / 16 : 0;
+  for (int64_t i = t0; i < nv; i += stride)
+    reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+  for (int64_t i = nv * 16 + t0; i < bytes; i += stride) dst[i] = src[i];
+}
+
+cudaError_t launch_copy_h2d(void* dst, const void* src, int64_t bytes, cudaStream_t st) {
+  if (bytes <= 0) return cudaSuccess;
+  int64_t blocks = (bytes / 16 + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > 148 * 4 ? 148 * 4 : blocks);
+  copy_h2d_kernel<<<int(blocks), 256, 0, st>>>(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+  return cudaPeekAtLastError();
+}
+
 }  // namespace rx

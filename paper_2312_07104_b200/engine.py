@@ -609,7 +609,7 @@ class Engine:
             sn[o2 + 2 * total:o2 + 3 * total] = new_slots
         else:
             sn[hdr:] = slots.reshape(-1)
-        dstage = stage.to(dev, non_blocking=True)
+        dstage = self._upload(stage)
         self._pinned_done(name)
         if incremental:
             d_idx = dstage[o2:o2 + 2 * total].view(torch.int64)
@@ -662,7 +662,7 @@ class Engine:
                 cn[o_ + 3 * n + 1:o_ + 4 * n + 1] = rows[b0:b1] if rows is not None else np.arange(b0, b1)
                 meta.append((o_, n))
                 o_ += 4 * n + 1
-            dchunk = cst.to(dev, non_blocking=True)
+            dchunk = self._upload(cst)
             self._pinned_done(cname)
             qo = np.concatenate([[0], np.cumsum(ext)])
             for (b0, b1), (c0, n) in zip(chunks, meta):
@@ -737,7 +737,7 @@ class Engine:
                        else api.rx_decode_workspace_bytes(self.cfg, int(B), int(ms)))
         # decode_bytes() needs (running, pos) per call, read after the timed region: copy the records
         sn = stage.numpy().copy() if self.timer is not None else None
-        d_all = stage.to(dev, non_blocking=True)
+        d_all = self._upload(stage)
         self._pinned_done(name)
         if need > self._ws.numel():
             self._ws = torch.zeros(2 * need, dtype=torch.uint8, device=dev)   # geometric growth
@@ -785,6 +785,14 @@ class Engine:
             self._tend(ev_run, "decode", works, nl_run, calls=len(meta))
 
     # ------------------------------------------------------------------ pinned staging
+    def _upload(self, stage):
+        """Device copy of a pinned staging slice, made by an SM kernel (rx_copy_h2d): metadata uploads
+        must not wait on the copy engines behind a large input prefetch (e2e path)."""
+        d = torch.empty(stage.shape, dtype=stage.dtype, device=self.device)
+        api.rx_copy_h2d(d, stage)
+        self.stats["launches"] += 1
+        return d
+
     def _pinned(self, name, n):
         """Pinned int32 staging buffer of >= n elements from a pool: the oldest buffer that is large
         enough and whose last H2D copy has completed is reused, so steady state allocates nothing —

@@ -55,5 +55,32 @@ def main():
               f"both {bw(both, 2 * tot):.1f} GB/s (sum)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and __import__("sys").argv[-1] != "load":
     main()
+
+
+def under_load():
+    """H2D of 1 GiB pinned while another stream saturates HBM with reads (torch sum over 8 GiB):
+    the rate the e2e path's input copies get while decode kernels run."""
+    dev = torch.device("cuda", 0)
+    h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    big = torch.ones(1 << 31, dtype=torch.float32, device=dev)
+    s_load, s_copy = torch.cuda.Stream(), torch.cuda.Stream()
+    for load in (False, True):
+        torch.cuda.synchronize()
+        if load:
+            with torch.cuda.stream(s_load):
+                for _ in range(40):
+                    big.sum()
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        with torch.cuda.stream(s_copy):
+            a.record()
+            d.copy_(h, non_blocking=True)
+            b.record()
+        torch.cuda.synchronize()
+        print(f"1 GiB H2D {'under HBM read load' if load else 'alone':20s}: {(1 << 30) / (a.elapsed_time(b) / 1000) / 1e9:.1f} GB/s")
+
+
+if __name__ == "__main__" and __import__("sys").argv[-1] == "load":
+    under_load()

@@ -64,6 +64,22 @@ def test_store_kv_bit_exact():
     assert kp[torch.from_numpy(untouched).cuda()].abs().sum().item() == 0
 
 
+def test_copy_h2d_bitwise():
+    """rx_copy_h2d (SM-driven upload of pinned host metadata): every byte arrives, for aligned and
+    unaligned sizes / offsets; pageable host memory is refused."""
+    rng = np.random.default_rng(2)
+    for n in (1, 15, 16, 4097, 3 << 20):
+        h = torch.from_numpy(rng.integers(0, 256, n + 3, dtype=np.uint8)).pin_memory()
+        for off in (0, 3):
+            src = h[off:off + n]
+            d = torch.empty(n, dtype=torch.uint8, device="cuda")
+            rx.rx_copy_h2d(d, src)
+            torch.cuda.synchronize()
+            assert torch.equal(d.cpu(), src)
+    with pytest.raises(ValueError):
+        rx.rx_copy_h2d(torch.empty(8, dtype=torch.uint8, device="cuda"), torch.zeros(8, dtype=torch.uint8))
+
+
 def test_store_kv_table_only():
     """rx_store_kv with null k / v and a table index (the engine's jump-forward output steps, whose
     K/V the following rx_extend stores): only the table entries are written, the pools are not."""
