@@ -37,18 +37,29 @@
 
 namespace rx {
 
-constexpr int kDecWarps = 4;
+constexpr int kDecWarps = 4;       // warps per CTA (long splits)
 constexpr int kBlk = 16;
 
-template <int HD, int STAGES_ = (HD == 128 ? 2 : 6)>
+// splits of at most this many tokens run 2-warp CTAs (RX_DECODE_SHORT overrides: A/B knob)
+static int short_chunk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RX_DECODE_SHORT");
+    v = e ? atoi(e) : 256;
+  }
+  return v;
+}
+
+template <int HD, int STAGES_ = (HD == 128 ? 2 : 6), int WARPS_ = kDecWarps>
 struct DecCfg {
   static constexpr int RB = HD * 2;                   // bytes per row
   static constexpr int BLK_BYTES = kBlk * RB;         // one K (or V) block
   static constexpr int STAGES = STAGES_;
+  static constexpr int WARPS = WARPS_;
   static constexpr int WARP_BYTES = STAGES * 2 * BLK_BYTES;
-  static constexpr int SMEM = kDecWarps * WARP_BYTES;
+  static constexpr int SMEM = WARPS * WARP_BYTES;
   static constexpr int CHUNKS = kBlk * HD / 8;        // 16-byte chunks per block
-  static_assert(SMEM >= kDecWarps * HD * 8 * 4, "merge scratch must fit");
+  static_assert(SMEM >= WARPS * HD * 8 * 4, "merge scratch must fit");
 };
 
 // slot > 0: pool row; slot == kNewTok: the step's own new token, read from the k_new / v_new
@@ -74,9 +85,9 @@ __device__ __forceinline__ void dec_issue_block(uint32_t kdst, uint32_t vdst, co
   }
 }
 
-template <int HD, int G, int STAGES, bool MULTI = false>
-__global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeParams p) {
-  using C = DecCfg<HD, STAGES>;
+template <int HD, int G, int STAGES, bool MULTI = false, int WARPS = kDecWarps>
+__global__ void __launch_bounds__(WARPS * 32, 2) decode_kernel(const DecodeParams p) {
+  using C = DecCfg<HD, STAGES, WARPS>;
   extern __shared__ __align__(128) uint8_t smem[];
   const int b = MULTI ? int(blockIdx.z) / p.col_tiles : int(blockIdx.z), g = blockIdx.y, s = blockIdx.x;
   // MULTI: this CTA's columns are ct*8 .. ct*8+7 of the request's nq*G (row, head) pairs
@@ -146,8 +157,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   auto vst = [&](int st) { return wbase + st * 2 * C::BLK_BYTES + C::BLK_BYTES; };
 
   const int nblk = (end - start + kBlk - 1) / kBlk;
-  const int my = warp < nblk ? (nblk - warp + kDecWarps - 1) / kDecWarps : 0;
-  auto tok0 = [&](int i) { return start + (warp + i * kDecWarps) * kBlk; };
+  const int my = warp < nblk ? (nblk - warp + WARPS - 1) / WARPS : 0;
+  auto tok0 = [&](int i) { return start + (warp + i * WARPS) * kBlk; };
   // block i is late if it holds a position >= stable: wait (whole warp) before its table reads
   auto late = [&](int i) { return i < my && tok0(i) + kBlk > stable; };
   auto load_slot = [&](int i) -> int {
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
   __syncthreads();  // all warps done with their pipelines: reuse smem for the merge
 
   float* opart = reinterpret_cast<float*>(smem);                  // [warps][HD][8]
-  __shared__ float red_m[kDecWarps][8], red_l[kDecWarps][8];
+  __shared__ float red_m[WARPS][8], red_l[WARPS][8];
   if (gq == 0) {
     red_m[warp][2 * tq] = m0;
     red_m[warp][2 * tq + 1] = m1;
@@ -275,15 +286,15 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2) decode_kernel(const DecodeP
     ow[(d + 8) * 8 + 2 * tq + 1] = oacc[mt][3];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < (MULTI ? 8 : G) * HD; idx += kDecWarps * 32) {
+  for (int idx = threadIdx.x; idx < (MULTI ? 8 : G) * HD; idx += WARPS * 32) {
     const int h = idx / HD, d = idx % HD;   // MULTI: h is the column
     if (MULTI && (ct * 8 + h) / G >= nq) continue;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, red_m[w][h]);
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, red_m[w][h]);
     float acc = 0.f, Ls = 0.f;
 #pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) {
+    for (int w = 0; w < WARPS; ++w) {
       const float f = fast_exp2(red_m[w][h] - M);
       Ls += f * red_l[w][h];
       acc += f * opart[(w * HD + d) * 8 + h];
@@ -415,13 +426,21 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cud
 
 template <int HD, int G, int STAGES>
 static cudaError_t launch_decode_t(const DecodeParams& p, int batch, cudaStream_t st, int* launches) {
-  using C = DecCfg<HD, STAGES>;
-  {
-    cudaError_t e = ensure_smem_attr(decode_kernel<HD, G, STAGES>, C::SMEM);
-    if (e != cudaSuccess) return e;
-  }
   dim3 grid(p.max_splits - p.split_base, p.h_kv, batch);   // suffix splits (cascade: shared partials come first)
-  cudaError_t e = launch_pdl(decode_kernel<HD, G, STAGES>, grid, dim3(kDecWarps * 32), C::SMEM, st, p);
+  cudaError_t e;
+  if (p.chunk <= short_chunk()) {
+    // short splits (a cascade suffix of ~100-300 tokens, early decode steps): 2 warps per CTA so
+    // twice as many CTAs are resident (one wave instead of two or three)
+    using C = DecCfg<HD, STAGES, 2>;
+    e = ensure_smem_attr(decode_kernel<HD, G, STAGES, false, 2>, C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(decode_kernel<HD, G, STAGES, false, 2>, grid, dim3(2 * 32), C::SMEM, st, p);
+  } else {
+    using C = DecCfg<HD, STAGES>;
+    e = ensure_smem_attr(decode_kernel<HD, G, STAGES>, C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(decode_kernel<HD, G, STAGES>, grid, dim3(kDecWarps * 32), C::SMEM, st, p);
+  }
   if (e != cudaSuccess) return e;
   *launches = 1;
   if (p.max_splits > 1 && p.split_base == 0) {   // cascade: the caller merges after the shared part
