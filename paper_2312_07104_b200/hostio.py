@@ -146,7 +146,15 @@ class _BlockPrefetcher:
 class HostInputs:
     """Drop-in for ``engine.InputBank`` with the tensors in pinned host memory."""
 
-    def __init__(self, bank, device, ext_depth=2, dec_block=16, dec_depth=4):
+    def __init__(self, bank, device, ext_depth=None, dec_block=None, dec_depth=None):
+        # ext_depth 1: the next turn's extend input is queued on the copy engines only when the
+        # host reaches that turn, i.e. AFTER the current turn's decode-input blocks (the engines
+        # serve copies in submission order); 2 (the next extend at once) measured 506 vs 483 ms
+        # per C3 pass with host I/O.  RX_EXT_DEPTH / RX_DEC_BLOCK / RX_DEC_DEPTH: A/B knobs.
+        import os
+        ext_depth = ext_depth if ext_depth is not None else int(os.environ.get("RX_EXT_DEPTH", "1"))
+        dec_block = dec_block if dec_block is not None else int(os.environ.get("RX_DEC_BLOCK", "16"))
+        dec_depth = dec_depth if dec_depth is not None else int(os.environ.get("RX_DEC_DEPTH", "8"))
         # one copy stream per call kind: a large extend prefetch (~1 GB for a C3 turn) must not
         # queue in front of the small per-step decode inputs that are needed first
         self.streams = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device))
