@@ -347,8 +347,23 @@ def test_cascade_decode_vs_oracle(h_q, h_kv, hd, B, shared, contig, q_scale):
     """rx_decode_cascade_append (shared prefix attended once on the tensor cores,
     suffixes by the decode kernel, LSE merge) against the fp64 oracle; the KV
     append (pool rows, req_to_token entries) is bit-identical to rx_decode_append."""
-    rng = np.random.default_rng(B * 31 + shared + hd)
-    suffix = [int(x) for x in rng.integers(1, 300, B)]          # >= 1: the new token is per-request
+    _cascade_decode_check(h_q, h_kv, hd, B, shared, contig, q_scale, 300)
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,B,shared,max_suffix", [
+    (64, 8, 128, 24, 2048, 3000),      # several suffix splits per request, ragged last splits
+    (32, 32, 128, 7, 512, 1200),       # few requests
+    (8, 2, 64, 33, 128, 700),          # hd 64 (6-stage rings)
+])
+def test_cascade_decode_long_suffix_vs_oracle(h_q, h_kv, hd, B, shared, max_suffix):
+    """Cascade step with long, ragged suffixes (several suffix splits per request, short last
+    splits, few units) — vs the fp64 oracle."""
+    _cascade_decode_check(h_q, h_kv, hd, B, shared, False, 1.0, max_suffix)
+
+
+def _cascade_decode_check(h_q, h_kv, hd, B, shared, contig, q_scale, max_suffix):
+    rng = np.random.default_rng(B * 31 + shared + hd + max_suffix)
+    suffix = [int(x) for x in rng.integers(1, max_suffix, B)]   # >= 1: the new token is per-request
     lens = [shared + s for s in suffix]
     S = shared + sum(suffix) + 64
     free = np.arange(1, S) if contig else rng.permutation(np.arange(1, S))
