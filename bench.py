@@ -609,9 +609,13 @@ def measure(name, steps, warmup, dev, rank, world, gather, flush, barrier, max_o
         d = {"ms_per_step": ms / steps, "calls_per_step": calls // steps, "launches_per_step": nl // steps,
              "tokens_per_s": phase_tokens.get(k_, 0) * steps / sec if sec > 0 else None}
         if k_ == "gather":
-            # TP output all-gather per attention call (kernel-only figures are the other entries)
+            # TP output all-gather (kernel-only figures are the other entries): per gather call, and
+            # per attention call (FusedGather: one barrier per decode run, the data moved by the
+            # attention epilogue's own stores)
+            att = sum(v_[2] for kk_, v_ in kern.items() if kk_ != "gather")
             d = {"ms_per_step": ms / steps, "calls_per_step": calls // steps,
-                 "us_per_call": ms * 1000.0 / max(1, calls)}
+                 "us_per_call": ms * 1000.0 / max(1, calls), "us_per_attention_call": ms * 1000.0 / max(1, att),
+                 "kind": type(gather).__name__ if gather is not None else None}
             kernels[k_] = d
             continue
         if k_ == "extend":

@@ -511,9 +511,11 @@ size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, 
  * output head shards.  Each rank allocates ONE zero-filled device buffer of
  * rx_tp_buffer_bytes(world, cap) bytes (cap = the largest shard in bytes, a
  * multiple of 16), exports it with rx_tp_ipc_handle (RX_TP_HANDLE_BYTES
- * opaque bytes), and maps every peer's buffer with rx_tp_ipc_open (on a
- * multi-GPU node: NVLink / NVSwitch peer memory; ranks may also share one
- * device).  rx_tp_allgather(d_src, bytes, peer_bufs, world, rank, cap, seq)
+ * opaque bytes) together with rx_tp_ipc_offset(d_buf) (the buffer's byte
+ * offset inside the allocation the handle names — a caching allocator may
+ * sub-allocate it; -1 on error), and maps every peer's buffer with
+ * rx_tp_ipc_open (+ that peer's offset; on a multi-GPU node: NVLink /
+ * NVSwitch peer memory; ranks may also share one device).  rx_tp_allgather(d_src, bytes, peer_bufs, world, rank, cap, seq)
  * then, in one kernel on the stream: stores this rank's shard d_src[0, bytes)
  * into every rank's buffer (P2P stores), publishes seq to every rank, and
  * waits for every rank's seq; when it completes the caller's own buffer holds
@@ -528,10 +530,40 @@ size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, 
 #define RX_TP_HANDLE_BYTES 64
 size_t rx_tp_buffer_bytes(int32_t world, int64_t cap);
 rx_status rx_tp_ipc_handle(void* d_buf, void* handle_out);
+int64_t rx_tp_ipc_offset(const void* d_buf);
 rx_status rx_tp_ipc_open(const void* handle, void** d_ptr);
 rx_status rx_tp_ipc_close(void* d_ptr);
 rx_status rx_tp_allgather(const void* d_src, int64_t bytes, void* const* peer_bufs, int32_t world, int32_t rank,
                           int64_t cap, int64_t seq, void* stream);
+
+/* TP decode step with the all-gather FUSED into the attention epilogue (A7 +
+ * A8 + A9; the north star's "single all-gather over NVLink reassembling
+ * outputs", done as the output stores themselves).  Semantics of
+ * rx_decode_cascade_append (shared_len > 0) or rx_decode_append (shared_len
+ * == 0) on this rank's heads (cfg->h_q local q heads, cfg->h_kv kv heads), but
+ * there is no d_o: the kernel that produces the final bf16 row of (request b,
+ * local q head h) stores it into EVERY rank's gathered output
+ * out->d_o[p] (p < out->world; [batch, out->h_q_total, head_dim] bf16 on rank
+ * p, mapped into this process: NVLink / NVSwitch peer memory via
+ * rx_tp_ipc_open, or this rank's own buffer) at row b, head
+ * out->head_offset + h.  No separate collective, kernel or copy.  A rank's
+ * gathered buffer is complete once every rank has issued its calls and an
+ * rx_tp_allgather(bytes = 0) barrier after them has completed on this rank
+ * (its flags publish "my stores are done" and wait for every peer's);
+ * buffers must not be reused by a peer's later call before this rank is done
+ * reading them (double-buffer across barriers).  RX_E_INVALID if out is null,
+ * world is outside [1, 8], a destination is null, or the heads do not fit. */
+typedef struct {
+  void* d_o[8];          /* rank p's gathered output buffer for this call (device address valid here) */
+  int32_t world;         /* destinations (ranks) */
+  int32_t h_q_total;     /* q heads per gathered row */
+  int32_t head_offset;   /* this rank's first q head in the gathered row */
+} rx_tp_out;
+rx_status rx_decode_append_tp(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
+                              const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                              int32_t max_seq_len, int32_t shared_len, const void* d_q, const void* d_k_new,
+                              const void* d_v_new, const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
+                              int64_t num_slots, const rx_tp_out* out, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Number of kernel launches the last successful rx_extend / rx_decode /
  * rx_store_kv call on this thread issued (for launch accounting). */

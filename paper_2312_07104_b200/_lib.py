@@ -29,6 +29,10 @@ class AttnCfg(C.Structure):
     _fields_ = [("h_q", i32), ("h_kv", i32), ("head_dim", i32), ("sm_scale", f32)]
 
 
+class TpOut(C.Structure):
+    _fields_ = [("d_o", vp * 8), ("world", i32), ("h_q_total", i32), ("head_offset", i32)]
+
+
 EVICT_CB = C.CFUNCTYPE(None, vp, P32, i64)
 EVICT_PATH_CB = C.CFUNCTYPE(None, vp, P32, i64, i64, P32, i64)
 STEP_EVENT_CB = C.CFUNCTYPE(None, vp, i32, P64, P32, i64)
@@ -91,10 +95,13 @@ SIGNATURES = {
     "rx_decode_cascade_append": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, i32, i32, vp, vp, vp, vp,
                                            vp, vp, i64, vp, vp, sz, vp]),
     "rx_decode_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32, i32]),
+    "rx_decode_append_tp": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, i32, i32, vp, vp, vp, vp,
+                                      vp, vp, i64, C.POINTER(TpOut), vp, sz, vp]),
     "rx_last_launch_count": (i32, []),
     "rx_copy_h2d": (C.c_int, [vp, vp, i64, vp]),
     "rx_tp_buffer_bytes": (sz, [i32, i64]),
     "rx_tp_ipc_handle": (C.c_int, [vp, vp]),
+    "rx_tp_ipc_offset": (i64, [vp]),
     "rx_tp_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
     "rx_tp_ipc_close": (C.c_int, [vp]),
     "rx_tp_allgather": (C.c_int, [vp, i64, C.POINTER(vp), i32, i32, i64, i64, vp]),

@@ -13,7 +13,7 @@ import json
 
 import numpy as np
 
-from ._lib import lib, AttnCfg, EVICT_CB, EVICT_PATH_CB, STEP_EVENT_CB, RxError, P32, P64
+from ._lib import lib, AttnCfg, TpOut, EVICT_CB, EVICT_PATH_CB, STEP_EVENT_CB, RxError, P32, P64
 
 _I32 = np.int32
 SCHED_POLICY = {"lspf": 0, "fcfs": 1, "random": 2}   # rx_sched_policy
@@ -469,6 +469,36 @@ def rx_decode_cascade_append(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int
                                       _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0],
                                       _dev(o, torch.bfloat16, "o"), _dev(ws, None, "ws"), ws_bytes, _stream(stream))
     _check(st, "rx_decode_cascade_append")
+
+
+def tp_out(dests, h_q_total: int, head_offset: int):
+    """rx_tp_out for rx_decode_append_tp: dests = device addresses (ints) of every rank's gathered
+    output buffer [batch, h_q_total, head_dim] bf16 for this call, in rank order."""
+    if not 1 <= len(dests) <= 8:
+        raise ValueError("tp_out: 1..8 destinations")
+    t = TpOut()
+    for i, d in enumerate(dests):
+        t.d_o[i] = int(d)
+    t.world, t.h_q_total, t.head_offset = len(dests), h_q_total, head_offset
+    return t
+
+
+def rx_decode_append_tp(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int, shared_len: int, q, k_new, v_new,
+                        new_slots, k_pool, v_pool, out, ws=None, stream=None, stable_lens=None):
+    """TP decode step whose epilogue stores the output rows into every rank's gathered buffer
+    (include/rx.h rx_decode_append_tp); `out` from tp_out()."""
+    import torch
+    batch = seq_lens.shape[0]
+    ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    st = lib.rx_decode_append_tp(C.byref(cfg), batch, _dev(rtt, torch.int32, "rtt"), rtt.shape[1],
+                                 _dev(rows, torch.int32, "rows"), _dev(seq_lens, torch.int32, "seq_lens"),
+                                 _dev(stable_lens, torch.int32, "stable_lens"), max_seq_len, shared_len,
+                                 _dev(q, torch.bfloat16, "q"),
+                                 _dev(k_new, torch.bfloat16, "k_new"), _dev(v_new, torch.bfloat16, "v_new"),
+                                 _dev(new_slots, torch.int32, "new_slots"), _dev(k_pool, torch.bfloat16, "k_pool"),
+                                 _dev(v_pool, torch.bfloat16, "v_pool"), k_pool.shape[0], C.byref(out),
+                                 _dev(ws, None, "ws"), ws_bytes, _stream(stream))
+    _check(st, "rx_decode_append_tp")
 
 
 def rx_copy_h2d(dst, src_pinned, stream=None):

@@ -95,13 +95,15 @@ static rx_status decode_impl(const rx_attn_cfg* cfg, int32_t batch, const int32_
                              const int32_t* d_rows, const int32_t* d_seq_lens, int32_t max_seq_len, const void* d_q,
                              const void* d_k_pool, const void* d_v_pool, int64_t num_slots, void* d_o, void* d_ws,
                              size_t ws_bytes, void* stream, const void* d_k_new, const void* d_v_new,
-                             const int32_t* d_new_slots, int32_t* d_rtt_w, const int32_t* d_stable_lens) {
+                             const int32_t* d_new_slots, int32_t* d_rtt_w, const int32_t* d_stable_lens,
+                             const rx::OutSpec* os = nullptr) {
   rx_status s = check_cfg(cfg);
   if (s != RX_OK) return s;
   if (batch < 0 || max_seq_len < 0 || num_slots < 1) return RX_E_INVALID;
   g_last_launches = 0;
   if (batch == 0) return RX_OK;
-  if (max_seq_len < 1 || !d_rtt || !d_seq_lens || !d_q || !d_k_pool || !d_v_pool || !d_o) return RX_E_INVALID;
+  if (max_seq_len < 1 || !d_rtt || !d_seq_lens || !d_q || !d_k_pool || !d_v_pool || (!d_o && !os))
+    return RX_E_INVALID;
   if (rtt_stride < max_seq_len) return RX_E_INVALID;
   const size_t need = rx::decode_ws_bytes(cfg->h_q, cfg->head_dim, batch, max_seq_len, cfg->h_kv);
   if (need > 0 && (!d_ws || ws_bytes < need)) return RX_E_WORKSPACE;
@@ -129,6 +131,7 @@ static rx_status decode_impl(const rx_attn_cfg* cfg, int32_t batch, const int32_
   p.new_slots = d_new_slots;
   p.rtt_w = d_rtt_w;
   p.stable_lens = d_stable_lens;
+  if (os) p.out = *os;
   int launches = 0;
   cudaError_t e = rx::launch_decode(cfg->head_dim, cfg->h_q / cfg->h_kv, p, batch,
                                     static_cast<cudaStream_t>(stream), &launches);
@@ -161,23 +164,25 @@ size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, 
   return rx::cascade_ws_bytes(cfg->h_q, cfg->head_dim, batch, cfg->h_kv, max_seq_len, shared_len);
 }
 
-rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
-                                   const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
-                                   int32_t max_seq_len,
-                                   int32_t shared_len, const void* d_q, const void* d_k_new, const void* d_v_new,
-                                   const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool, int64_t num_slots,
-                                   void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
+static rx_status cascade_impl(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
+                              const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                              int32_t max_seq_len, int32_t shared_len, const void* d_q, const void* d_k_new,
+                              const void* d_v_new, const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
+                              int64_t num_slots, void* d_o, void* d_ws, size_t ws_bytes, void* stream,
+                              const rx::OutSpec* os) {
   rx_status s = check_cfg(cfg);
   if (s != RX_OK) return s;
   if (batch < 0 || num_slots < 1 || shared_len < 0) return RX_E_INVALID;
   g_last_launches = 0;
   if (batch == 0) return RX_OK;
-  if (shared_len == 0)   // nothing shared: the ordinary fused path
-    return rx_decode_append(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, d_stable_lens, max_seq_len, d_q,
-                            d_k_new, d_v_new, d_new_slots, d_k_pool, d_v_pool, num_slots, d_o, d_ws, ws_bytes,
-                            stream);
+  if (shared_len == 0) {  // nothing shared: the ordinary fused path
+    if (!d_k_new || !d_v_new || !d_new_slots) return RX_E_INVALID;
+    return decode_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, max_seq_len, d_q, d_k_pool, d_v_pool,
+                       num_slots, d_o, d_ws, ws_bytes, stream, d_k_new, d_v_new, d_new_slots, d_rtt, d_stable_lens,
+                       os);
+  }
   if (max_seq_len <= shared_len || !d_rtt || !d_seq_lens || !d_q || !d_k_new || !d_v_new || !d_new_slots ||
-      !d_k_pool || !d_v_pool || !d_o || rtt_stride < max_seq_len)
+      !d_k_pool || !d_v_pool || (!d_o && !os) || rtt_stride < max_seq_len)
     return RX_E_INVALID;
   const int G = cfg->h_q / cfg->h_kv;
   const size_t need = rx::cascade_ws_bytes(cfg->h_q, cfg->head_dim, batch, cfg->h_kv, max_seq_len, shared_len);
@@ -244,10 +249,44 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
   ep.cas_chunk = pl.suffix.chunk;
   ep.pdl = rx::pdl_on();
   ep.sched = static_cast<int*>(d_ws);
+  if (os) ep.out = *os;
   e = rx::launch_extend_cascade(cfg->head_dim, G, ep, d_q, batch, st);
   if (e != cudaSuccess) return RX_E_CUDA;
   g_last_launches = launches + 2;
   return RX_OK;
+}
+
+rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
+                                   const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                                   int32_t max_seq_len,
+                                   int32_t shared_len, const void* d_q, const void* d_k_new, const void* d_v_new,
+                                   const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool, int64_t num_slots,
+                                   void* d_o, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_o) return RX_E_INVALID;
+  return cascade_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, d_stable_lens, max_seq_len, shared_len,
+                      d_q, d_k_new, d_v_new, d_new_slots, d_k_pool, d_v_pool, num_slots, d_o, d_ws, ws_bytes, stream,
+                      nullptr);
+}
+
+rx_status rx_decode_append_tp(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
+                              const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
+                              int32_t max_seq_len, int32_t shared_len, const void* d_q, const void* d_k_new,
+                              const void* d_v_new, const int32_t* d_new_slots, void* d_k_pool, void* d_v_pool,
+                              int64_t num_slots, const rx_tp_out* out, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!out || out->world < 1 || out->world > rx::kTpMaxRanks || !cfg || out->head_offset < 0 ||
+      out->h_q_total < out->head_offset + cfg->h_q)
+    return RX_E_INVALID;
+  rx::OutSpec os{};
+  for (int i = 0; i < out->world; ++i) {
+    if (!out->d_o[i]) return RX_E_INVALID;
+    os.ptr[i] = static_cast<__nv_bfloat16*>(out->d_o[i]);
+  }
+  os.n = out->world;
+  os.head_off = out->head_offset;
+  os.row_stride = int64_t(out->h_q_total) * cfg->head_dim;
+  return cascade_impl(cfg, batch, d_rtt, rtt_stride, d_rows, d_seq_lens, d_stable_lens, max_seq_len, shared_len,
+                      d_q, d_k_new, d_v_new, d_new_slots, d_k_pool, d_v_pool, num_slots, nullptr, d_ws, ws_bytes,
+                      stream, &os);
 }
 
 // Multi-query cascade (rx_extend_cascade): rows = every new token of the batch.

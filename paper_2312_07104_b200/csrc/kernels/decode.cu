@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) decode_kernel(const DecodeParam
     }
     const int hq = g * G + h;
     if (nsplit == 1 && p.split_base == 0) {
-      p.o[(int64_t(b) * p.h_q + hq) * HD + d] = __float2bfloat16_rn(acc / Ls);
+      out_put(p.out, p.o, p.h_q, HD, b, hq, d, __float2bfloat16_rn(acc / Ls));
     } else {
       const int64_t base = (int64_t(b) * p.h_q + hq) * p.max_splits + p.split_base + s;
       p.ws_o[base * HD + d] = acc / Ls;
@@ -373,10 +373,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const De
     }
   }
   const float inv = 1.f / W;
-  __nv_bfloat16* dst = p.o + pair * HD + lane * V;
+  const int hq = int(pair - int64_t(b) * p.h_q);
 #pragma unroll
   for (int v = 0; v < V; v += 2)
-    *reinterpret_cast<uint32_t*>(dst + v) = pack_bf16(acc[v] * inv, acc[v + 1] * inv);
+    out_put(p.out, p.o, p.h_q, HD, b, hq, lane * V + v, pack_bf16(acc[v] * inv, acc[v + 1] * inv));
 }
 
 static dim3 merge_grid(int rows, int h_q) {

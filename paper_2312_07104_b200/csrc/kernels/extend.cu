@@ -818,9 +818,9 @@ __global__ void __launch_bounds__(kCasMergeWarps * 32) cascade_merge_kernel(cons
     }
   }
   const float inv = 1.f / W;
-  __nv_bfloat16* dst = p.o + pair * HD + lane * V;
 #pragma unroll
-  for (int v = 0; v < V; v += 2) *reinterpret_cast<uint32_t*>(dst + v) = pack_bf16(acc[v] * inv, acc[v + 1] * inv);
+  for (int v = 0; v < V; v += 2)
+    out_put(p.out, p.o, p.h_q, HD, row, hq, lane * V + v, pack_bf16(acc[v] * inv, acc[v + 1] * inv));
 }
 
 template <int HD>

@@ -59,6 +59,30 @@ inline int device_sms() {
 constexpr int kTpMaxRanks = 8;
 constexpr int64_t kTpHeader = 256;
 
+// Where a call's final bf16 output rows go (rx_decode_append_tp, include/rx.h section 3): n == 0
+// -> the call's own o [rows, h_q, HD]; n > 0 -> row b, local head h of EVERY destination ptr[i]
+// (each rank's gathered buffer, peer-mapped) at b * row_stride + (head_off + h) * HD: the TP
+// all-gather done by the epilogue's stores.
+struct OutSpec {
+  __nv_bfloat16* ptr[kTpMaxRanks];
+  int n;
+  int head_off;
+  int64_t row_stride;     // elements per gathered row (h_q_total * HD)
+};
+
+// Store a value of type T (bf16, or a packed pair) at head dim d of output row b, local head hq.
+template <typename T>
+__device__ __forceinline__ void out_put(const OutSpec& os, __nv_bfloat16* o, int h_q, int hd, int64_t b, int hq,
+                                        int d, T v) {
+  if (os.n == 0) {
+    *reinterpret_cast<T*>(o + (b * h_q + hq) * hd + d) = v;
+    return;
+  }
+  const int64_t off = b * os.row_stride + int64_t(os.head_off + hq) * hd + d;
+#pragma unroll 1
+  for (int i = 0; i < os.n; ++i) *reinterpret_cast<T*>(os.ptr[i] + off) = v;
+}
+
 struct DecodeParams {
   const __nv_bfloat16* q;       // [B, h_q, HD]
   const __nv_bfloat16* kpool;   // [S, h_kv, HD]
@@ -96,6 +120,7 @@ struct DecodeParams {
   const int32_t* qo_indptr;
   const int32_t* prefix_lens;
   int col_tiles;
+  OutSpec out;                  // final output rows (non-MULTI); n == 0: o
 };
 
 struct ExtendParams {
@@ -142,6 +167,7 @@ struct ExtendParams {
   // (hence the previous step, whose reads of the workspace are done) before writing partials
   int pdl;
   int* sched;                   // [2] work counters: the caller's workspace header (kWsHeader)
+  OutSpec out;                  // cascade merge output rows (decode steps); n == 0: o
 };
 
 struct DecodePlan {

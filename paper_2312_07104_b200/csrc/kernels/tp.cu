@@ -14,6 +14,7 @@
 // runs call seq + 1 never overwrites the slot this rank still reads for call seq (it cannot reach
 // seq + 2 before this rank signalled seq + 1, which is after this rank's reads of seq in stream
 // order).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -87,6 +88,26 @@ rx_status rx_tp_ipc_handle(void* d_buf, void* handle_out) {
   static_assert(sizeof(h) == RX_TP_HANDLE_BYTES, "IPC handle size");
   memcpy(handle_out, &h, sizeof(h));
   return RX_OK;
+}
+
+int64_t rx_tp_ipc_offset(const void* d_buf) {
+  // an IPC handle names the whole allocation that holds d_buf (a caching allocator may place the
+  // buffer inside a larger segment): peers add this offset to the base they open
+  typedef CUresult (*GetRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRangeFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return -1;
+    fn = reinterpret_cast<GetRangeFn>(ptr);
+  }
+  if (!d_buf) return -1;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(d_buf)) != CUDA_SUCCESS) return -1;
+  return int64_t(reinterpret_cast<CUdeviceptr>(d_buf) - base);
 }
 
 rx_status rx_tp_ipc_open(const void* handle, void** d_ptr) {

@@ -744,17 +744,36 @@ class Engine:
         # timing: one event pair around the whole run of back-to-back decode calls (per-call events
         # on ~2000 calls per C3 step would perturb the step); per call when outputs are gathered
         # (TP), so the all-gather stays outside the kernel brackets
-        per_call = self.gather is not None
+        # TP with the gather fused into the epilogue (tp.FusedGather): the calls store straight into
+        # every rank's gathered buffer; one flag barrier ends the run, then the outputs are read
+        fused = getattr(self.gather, "fused", False)
+        per_call = self.gather is not None and not fused
         ev_run = None if per_call else self._tbeg()
-        works, nl_run = [], 0
+        works, nl_run, pending = [], 0, []
+        if fused:
+            self.gather.begin_run()
         for B, o0, max_seq in meta:
             B, o0, max_seq = int(B), int(o0), int(max_seq)
             q, k, v = self.bank.dec[self._dec_i]
             self._dec_i += 1
             d = d_all[o0:o0 + 4 * B]
-            o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
             ev0 = self._tbeg() if per_call else None
-            if sh:
+            if fused:
+                hq_all, hd = self.shape.h_q, self.shape.head_dim
+                if not self.gather.fits(B, hq_all, hd):   # region full: end the run, start the next
+                    self._fused_end_run(pending)
+                    pending = []
+                    self.gather.begin_run()
+                dests, o = self.gather.take(B, hq_all, hd)
+                out = api.tp_out(dests, hq_all, int(self.heads_q[0]))
+                api.rx_decode_append_tp(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, sh, q, k, v,
+                                        d[:B], self.k_pool, self.v_pool, out, self._ws,
+                                        stable_lens=None if sh else d[3 * B:])
+            else:
+                o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
+            if fused:
+                pass
+            elif sh:
                 # (no stable region: in the cascade chain the early release measured slower, C5 step
                 # 101 -> 140 us, because the tcgen05 shared-prefix kernel needs whole SMs)
                 api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, sh, q, k, v,
@@ -772,6 +791,9 @@ class Engine:
                     self._tend(ev0, "decode", [w], nl)
                 works.append(w)
             nl_run += nl
+            if fused:
+                pending.append((o, B))
+                continue
             if self.gather is not None:
                 evg = self._tbeg()
                 o = self.gather(o)
@@ -783,6 +805,24 @@ class Engine:
                 self.outputs.append(("decode", o, {"B": B}))
         if ev_run is not None:
             self._tend(ev_run, "decode", works, nl_run, calls=len(meta))
+        if fused:
+            self._fused_end_run(pending)
+
+    def _fused_end_run(self, pending):
+        """End a FusedGather run: the host sink's copies of the previous run are done (a peer may
+        overwrite that region after this barrier), the barrier (every rank's stores of this run are
+        visible here), then this run's gathered outputs go to the sink / the kept outputs."""
+        if self.sink is not None and hasattr(self.sink, "join"):
+            self.sink.join()
+        evg = self._tbeg()
+        self.gather.end_run()
+        if evg is not None:
+            self._tend(evg, "gather", 0.0, 1)
+        for o, B in pending:
+            if self.sink is not None:
+                self.sink("decode", o)
+            if self.keep_outputs:
+                self.outputs.append(("decode", o.clone(), {"B": B}))
 
     # ------------------------------------------------------------------ pinned staging
     def _upload(self, stage):

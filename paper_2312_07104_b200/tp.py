@@ -9,11 +9,14 @@ same."  So:
   hash of the tree to prove it);
 * rank r owns q heads [r*H_q/P, (r+1)*H_q/P) and the kv heads they read, i.e.
   its slice of the pool (``engine.shard_heads``);
-* the only exchange is ONE all-gather of the bf16 attention output per call:
-  NCCL ``all_gather_into_tensor`` (``Gather``, default), or ``P2PGather``
-  (librx rx_tp_allgather: one kernel stores the shard into every peer's
-  IPC-mapped buffer over NVLink and synchronises with flags; opt-in,
-  RX_TP_P2P=1), with NCCL for the chunked, overlapped extend gathers.
+* the only exchange is ONE all-gather of the bf16 attention output per call.
+  Decode steps (thousands per C3 step): ``FusedGather`` (default on a CUDA
+  group) — the attention epilogue stores every output row into every rank's
+  IPC-mapped buffer (rx_decode_append_tp), one flag barrier per decode run;
+  no collective per step.  Otherwise NCCL ``all_gather_into_tensor``
+  (``Gather``), or ``P2PGather`` (librx rx_tp_allgather: one kernel stores the
+  shard into every peer's buffer and synchronises with flags; RX_TP_P2P=1);
+  extend calls use NCCL (chunked, overlapped with the next block's compute).
 """
 from __future__ import annotations
 
@@ -22,6 +25,31 @@ import json
 
 import torch
 import torch.distributed as dist
+
+
+def _map_peers(lib, buf, world, rank, group):
+    """Export this rank's buffer (IPC handle + its offset inside the handle's allocation) and map
+    every peer's: (opened base pointers to close later, [device address of rank r's buffer])."""
+    import ctypes as C
+    h = (C.c_uint8 * 64)()
+    st = lib.rx_tp_ipc_handle(C.c_void_p(buf.data_ptr()), C.cast(h, C.c_void_p))
+    off = lib.rx_tp_ipc_offset(C.c_void_p(buf.data_ptr()))
+    if st != 0 or off < 0:
+        raise RuntimeError(f"rx_tp_ipc_handle / rx_tp_ipc_offset: {st} / {off}")
+    handles = [None] * world
+    dist.all_gather_object(handles, (bytes(h), int(off)), group=group)
+    opened, ptrs = [], []
+    for r, (hb, o) in enumerate(handles):
+        if r == rank:
+            ptrs.append(buf.data_ptr())
+            continue
+        p = C.c_void_p()
+        st = lib.rx_tp_ipc_open(C.cast((C.c_uint8 * 64).from_buffer_copy(hb), C.c_void_p), C.byref(p))
+        if st != 0:
+            raise RuntimeError(f"rx_tp_ipc_open(rank {r}): {st}")
+        opened.append(p)
+        ptrs.append(p.value + o)
+    return opened, ptrs
 
 
 class Gather:
@@ -83,25 +111,7 @@ class P2PGather:
         self.cap = (int(cap_bytes) + 15) // 16 * 16
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.buf = torch.zeros(int(lib.rx_tp_buffer_bytes(self.world, self.cap)), dtype=torch.uint8, device=dev)
-        h = (C.c_uint8 * 64)()
-        st = lib.rx_tp_ipc_handle(C.c_void_p(self.buf.data_ptr()), C.cast(h, C.c_void_p))
-        if st != 0:
-            raise RuntimeError(f"rx_tp_ipc_handle: {st}")
-        handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(h), group=group)
-        self._opened = []
-        ptrs = []
-        for r, hb in enumerate(handles):
-            if r == self.rank:
-                ptrs.append(self.buf.data_ptr())
-                continue
-            p = C.c_void_p()
-            hh = (C.c_uint8 * 64).from_buffer_copy(hb)
-            st = lib.rx_tp_ipc_open(C.cast(hh, C.c_void_p), C.byref(p))
-            if st != 0:
-                raise RuntimeError(f"rx_tp_ipc_open(rank {r}): {st}")
-            self._opened.append(p)
-            ptrs.append(p.value)
+        self._opened, ptrs = _map_peers(lib, self.buf, self.world, self.rank, group)
         self.peers = (C.c_void_p * self.world)(*ptrs)
         self.seq = 0
         self.fallback = Gather(group)
@@ -141,7 +151,100 @@ class P2PGather:
         self._opened = []
 
 
-def make_gather(group=None, p2p=None):
+class FusedGather:
+    """Decode outputs gathered by the attention epilogue itself (include/rx.h rx_decode_append_tp):
+    the kernel that produces a final output row stores it into EVERY rank's gathered buffer over
+    peer memory, so a decode step has no collective, no extra kernel and no copy.
+
+    Every rank holds one IPC buffer: [256-byte barrier header | region 0 | region 1] (regions of
+    ``region_bytes``, holding gathered rows [h_q_total, head_dim] bf16); every rank maps every
+    peer's buffer.
+    A decode run (the calls of one engine decode launch) takes consecutive rows of region
+    (run & 1) — the same rows on every rank, because every rank issues the identical call
+    sequence — and ends with ONE rx_tp_allgather(bytes = 0) barrier: its flags publish "my stores
+    of this run are done" and wait for every peer's, after which this rank's region holds the
+    whole gathered output of the run.  A peer writes region (run & 1) again only in run + 2,
+    i.e. after this rank's barrier of run + 1, which the engine issues only once its readers of
+    run (the host sink's copies) are done.  Extend calls (few, large) use NCCL (``Gather``)."""
+
+    fused = True
+
+    def __init__(self, region_bytes=256 << 20, group=None, device=None, fallback=None, host_barrier=False):
+        import ctypes as C
+        from ._lib import lib
+        self._lib, self._C = lib, C
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.region_bytes = (int(region_bytes) + 255) // 256 * 256
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.buf = torch.zeros(256 + 2 * self.region_bytes, dtype=torch.uint8, device=dev)
+        self._opened, ptrs = _map_peers(lib, self.buf, self.world, self.rank, group)
+        self.ptrs = ptrs
+        self.peers = (C.c_void_p * self.world)(*ptrs)
+        self.run = 0
+        self.used = 0
+        self.seq = 0
+        self.fallback = fallback if fallback is not None else Gather(group)
+        # host_barrier (tests with several ranks on ONE device): end a run by synchronising this
+        # rank's device and a process-group barrier instead of the device flag barrier — ranks that
+        # time-share one GPU must not spin in a kernel on work of a context that is not running
+        # (one process per GPU, the deployment, uses the device barrier)
+        self.host_barrier = host_barrier
+        dist.barrier(group=group)              # every rank mapped every buffer before the first call
+
+    def begin_run(self):
+        self.run += 1
+        self.used = 0
+
+    def fits(self, rows, h_q_total, head_dim):
+        return self.used + (rows * h_q_total * head_dim * 2 + 255) // 256 * 256 <= self.region_bytes
+
+    def take(self, rows, h_q_total, head_dim):
+        """(destination addresses on every rank, this rank's view [rows, h_q_total, head_dim]) of
+        the next gathered block of the current run."""
+        n = rows * h_q_total * head_dim * 2
+        if not self.fits(rows, h_q_total, head_dim):
+            raise RuntimeError(f"FusedGather: run exceeds {self.region_bytes} bytes (end the run first)")
+        off = 256 + (self.run & 1) * self.region_bytes + self.used
+        self.used += (n + 255) // 256 * 256
+        view = self.buf[off:off + n].view(torch.bfloat16).view(rows, h_q_total, head_dim)
+        return [p + off for p in self.ptrs], view
+
+    def end_run(self):
+        """The run's barrier on the current stream (every rank's stores of the run are visible)."""
+        self.seq += 1
+        if self.host_barrier:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+            return
+        C = self._C
+        st = self._lib.rx_tp_allgather(None, 0, self.peers, self.world, self.rank, 16, self.seq,
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if st != 0:
+            raise RuntimeError(f"rx_tp_allgather (barrier): {st}")
+
+    # extend calls: NCCL
+    def __call__(self, o_local):
+        return self.fallback(o_local)
+
+    def alloc(self, n, hq_local, hd, dtype, device):
+        return self.fallback.alloc(n, hq_local, hd, dtype, device)
+
+    def start(self, o_part, out, r0, r1):
+        return self.fallback.start(o_part, out, r0, r1)
+
+    @staticmethod
+    def finish(handles, out):
+        return Gather.finish(handles, out)
+
+    def close(self):
+        for p in self._opened:
+            self._lib.rx_tp_ipc_close(p)
+        self._opened = []
+
+
+def make_gather(group=None, p2p=None, fused=None):
     """The TP output gather: NCCL (Gather) by default; the peer-memory P2PGather when p2p=True or
     RX_TP_P2P=1 on a CUDA (NCCL) group.  (Measured on one rank: NCCL's gather costs 7 us of device
     time per call, P2PGather 21 us — its kernel + copy + launch — so P2P is opt-in until a fused
@@ -149,7 +252,12 @@ def make_gather(group=None, p2p=None):
     import os
     if p2p is None:
         p2p = os.environ.get("RX_TP_P2P", "0") == "1"
-    if p2p and dist.get_backend(group) == "nccl":
+    if fused is None:
+        fused = os.environ.get("RX_TP_FUSED", "1") == "1"
+    nccl = dist.get_backend(group) == "nccl"
+    if fused and nccl:
+        return FusedGather(group=group)
+    if p2p and nccl:
         return P2PGather(group=group)
     return Gather(group)
 

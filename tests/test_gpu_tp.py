@@ -61,10 +61,13 @@ def test_fake_tp_matches_single_gpu(make, P):
     assert oe.trace == full.trace
 
 
-def test_chunked_overlapped_gather_world1_nccl():
+@pytest.mark.parametrize("fused", [True, False])
+def test_chunked_overlapped_gather_world1_nccl(fused):
     """The TP extend path with the output all-gather split into request blocks and overlapped with
     the next block's compute (NCCL async, one-rank group on this GPU): outputs are bit-identical to
-    the unchunked call (blocks never split a request; each request's math is unchanged)."""
+    the unchunked call (blocks never split a request; each request's math is unchanged).  fused:
+    decode steps through tp.FusedGather (rx_decode_append_tp: the epilogue stores into the gathered
+    buffer, one barrier per decode run), else one NCCL all-gather per decode call."""
     import os
     import socket
     import torch.distributed as dist
@@ -80,7 +83,9 @@ def test_chunked_overlapped_gather_world1_nccl():
     wl = workloads.c5(n_req=12, prefix=600, question=40, decode=3, num_slots=16384, ragged=True)
     ref = _run(wl)
     _, bank = plan_and_bank(wl, "cuda")
-    e = Engine(wl, "cuda", record=True, keep_outputs=True, gather=make_gather())
+    g = make_gather(fused=fused)
+    assert type(g).__name__ == ("FusedGather" if fused else "Gather")
+    e = Engine(wl, "cuda", record=True, keep_outputs=True, gather=g)
     e.gather_chunk_rows = 100                       # several blocks for the 12 x U[64,256]-row extend
     assert e._gather_chunks(np.array([150] * 12)) is not None
     e.run_workload(bank)
@@ -89,4 +94,7 @@ def test_chunked_overlapped_gather_world1_nccl():
     for (k1, o1, _), (k2, o2, _) in zip(ref.outputs, e.outputs):
         assert k1 == k2
         assert torch.equal(o1, o2.reshape(o1.shape))
+    if fused:
+        assert g.seq > 0                            # decode runs ended with their barriers
+        g.close()
     dist.destroy_process_group()

@@ -52,6 +52,14 @@ def _worker(rank, world, port, wl_args, q, kind="host"):
         if kind == "p2p":
             from paper_2312_07104_b200.tp import P2PGather
             gather = P2PGather(cap_bytes=4 << 20)
+        elif kind == "fused":
+            # decode outputs stored by the attention epilogue into both ranks' IPC-mapped buffers
+            # (rx_decode_append_tp), one flag barrier per decode run; extends through host copies;
+            # small regions so runs also end early (region full) mid-phase
+            from paper_2312_07104_b200.tp import FusedGather
+            # (runs end with a host barrier: two processes time-sharing one device cannot spin on each
+            # other's flags in a kernel; the device flag barrier is covered by the P2P test below)
+            gather = FusedGather(region_bytes=1 << 20, fallback=_HostGather(dist), host_barrier=True)
         else:
             gather = _HostGather(dist)
         e = Engine(wl, "cuda", tp_rank=rank, tp_size=world, record=True, keep_outputs=True, gather=gather)
@@ -72,10 +80,13 @@ def _worker(rank, world, port, wl_args, q, kind="host"):
     # two processes' contexts); the C3 case of this mode trapped on its 30 s peer wait in one run
     # (open) and is not part of the suite
     (("c5", dict(n_req=6, prefix=600, question=40, decode=5, num_slots=8192)), "p2p"),
+    (("c5", dict(n_req=6, prefix=600, question=40, decode=5, num_slots=8192)), "fused"),   # cascade + fused
+    (("c3", dict(sessions=4, turns=2, in_lo=30, in_hi=90, out_lo=4, out_hi=9, num_slots=8192)), "fused"),
 ])
 def test_tp2_processes_gathered_outputs_vs_oracle(wl_args, kind):
     """kind = host: gloo all-gather through host copies; p2p: librx rx_tp_allgather (each rank's
-    kernel stores its shard into the peer's IPC-mapped buffer and synchronises by flags)."""
+    kernel stores its shard into the peer's IPC-mapped buffer and synchronises by flags); fused:
+    the decode kernels' epilogues store into both ranks' buffers (tp.FusedGather)."""
     from oracle.driver import OracleEngine
     from rxgen import workloads
     ctx = mp.get_context("spawn")
@@ -84,7 +95,7 @@ def test_tp2_processes_gathered_outputs_vs_oracle(wl_args, kind):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, wl_args, q, kind), daemon=True) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
+    res = [q.get(timeout=300) for _ in range(2)]
     for p in procs:
         p.join(timeout=60)
     res.sort(key=lambda r: r[0])
@@ -102,7 +113,7 @@ def test_tp2_processes_gathered_outputs_vs_oracle(wl_args, kind):
     outs = res[0][2]
     ext = [x for x in outs if x[0] == "extend"]
     dec = [x for x in outs if x[0] == "decode"]
-    errs = []
+    errs, worst = [], []
     for key, ref in oe.outputs.items():
         if key[0] == "extend":
             _, call, bi, j = key
@@ -110,9 +121,12 @@ def test_tp2_processes_gathered_outputs_vs_oracle(wl_args, kind):
         else:
             got = dec[key[1]][1][key[2]]
         errs.append(np.abs(got.astype(np.float64) - ref).ravel())
+        e2 = np.abs(got.astype(np.float64) - ref).reshape(ref.shape[0], -1).max(1)
+        worst.append((float(e2.max()), key, [int(h) for h in np.nonzero(e2 > 2e-2)[0][:8]]))
     err = np.concatenate(errs)
     assert len(errs) > 100 and np.isfinite(err).all()
-    assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
+    worst.sort(reverse=True, key=lambda w: w[0])
+    assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean(), worst[:6])
 
 
 def _p2p_worker(rank, world, port, q):
