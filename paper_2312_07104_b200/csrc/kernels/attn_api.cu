@@ -219,6 +219,14 @@ static rx_status cascade_impl(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_
   dp.kv_start = shared_len;
   dp.split_base = pl.n_sh;
   dp.stable_lens = d_stable_lens;
+  // the shared pass launched next needs whole SMs: release it after the suffix streaming
+  // (RX_CASCADE_EARLY=1: as soon as every suffix CTA has started — A/B knob)
+  static int early = -1;
+  if (early < 0) {
+    const char* ev = getenv("RX_CASCADE_EARLY");
+    early = ev ? atoi(ev) : 0;
+  }
+  dp.late_trigger = early ? 0 : 1;
   int launches = 0;
   cudaError_t e = rx::launch_decode(cfg->head_dim, G, dp, batch, st, &launches);
   if (e != cudaSuccess) return RX_E_CUDA;

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) decode_kernel(const DecodeParam
   // with a stable region the next step is released as soon as every CTA has started (it reads only
   // its own stable positions before its wait); without one, after this CTA's streaming (the old
   // schedule: the cascade chain's tcgen05 partial kernel needs whole SMs and must not be delayed)
-  const bool early_trigger = !MULTI && p.stable_lens != nullptr;
+  const bool early_trigger = !MULTI && p.stable_lens != nullptr && !p.late_trigger;
   if (early_trigger) pdl_launch_dependents();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

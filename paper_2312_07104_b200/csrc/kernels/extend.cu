@@ -255,6 +255,10 @@ __device__ __forceinline__ void load_kv_tile(const ExtItem& I, int j, const Tile
 // slot (the softmax warps are issue-bound).  MUFU ex2 is the other limiter (16/clk/SM vs 8192 MMA
 // FLOP/clk): with POLY (an unmasked tile) every 4th column pair is evaluated on the FMA pipe
 // instead (exp2_poly3; masked tiles need exact zeros, so MUFU only).
+#ifndef RX_EXT_POLY_EVERY
+#define RX_EXT_POLY_EVERY 4     // every RX_EXT_POLY_EVERY-th column pair on the FMA pipe (A/B build knob)
+#endif
+
 template <bool POLY>
 __device__ __forceinline__ void softmax_half(const float* sv, int half, float sc, float nm, uint64_t* rs,
                                              uint32_t t_s) {
@@ -265,7 +269,7 @@ __device__ __forceinline__ void softmax_half(const float* sv, int half, float sc
     const int col = half * (kBN / 2) + 2 * c;
     float x0, x1, e0, e1;
     f2_unpack(f2_fma(f2_pack(sv[col], sv[col + 1]), sc2, nm2), x0, x1);
-    if (POLY && (c & 3) == 3) {
+    if (POLY && c % RX_EXT_POLY_EVERY == RX_EXT_POLY_EVERY - 1) {
       exp2_poly3_x2(x0, x1, e0, e1);
     } else {
       e0 = fast_exp2(x0);

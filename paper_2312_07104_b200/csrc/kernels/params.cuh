@@ -113,6 +113,9 @@ struct DecodeParams {
   // nullable: positions < stable_lens[b] were written before the decode phase (by plain-launched
   // kernels) and may be read before the programmatic-dependency wait
   const int32_t* stable_lens;
+  // with stable_lens: release the dependent grid only after this CTA's streaming (the cascade
+  // chain, whose next kernel needs whole SMs), not as soon as every CTA has started
+  int late_trigger;
   // multi-query mode (rx_extend with short segments, decode_kernel<..., MULTI>): request b owns
   // query rows qo_indptr[b] .. qo_indptr[b+1] (q / o ragged [N, h_q, HD]) at positions
   // prefix_lens[b] + j; causal inside the segment; CTA z = b * col_tiles + tile of 8 columns

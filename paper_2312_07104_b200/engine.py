@@ -49,6 +49,10 @@ class OutOfSlots(RuntimeError):
     pass
 
 
+# RX_CASCADE_STABLE=0: cascade decode steps without a stable region (A/B knob)
+_NO_CAS_STABLE = os.environ.get("RX_CASCADE_STABLE", "1") == "0"
+
+
 def shard_heads(h_q: int, h_kv: int, rank: int, size: int):
     """(q heads, kv heads) owned by this TP rank; kv heads replicated when size > h_kv."""
     assert h_q % size == 0, "h_q must divide by the TP size"
@@ -767,17 +771,18 @@ class Engine:
                 dests, o = self.gather.take(B, hq_all, hd)
                 out = api.tp_out(dests, hq_all, int(self.heads_q[0]))
                 api.rx_decode_append_tp(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, sh, q, k, v,
-                                        d[:B], self.k_pool, self.v_pool, out, self._ws,
-                                        stable_lens=None if sh else d[3 * B:])
+                                        d[:B], self.k_pool, self.v_pool, out, self._ws, stable_lens=d[3 * B:])
             else:
                 o = torch.empty((B, self.hq, self.shape.head_dim), dtype=torch.bfloat16, device=dev)
             if fused:
                 pass
             elif sh:
-                # (no stable region: in the cascade chain the early release measured slower, C5 step
-                # 101 -> 140 us, because the tcgen05 shared-prefix kernel needs whole SMs)
+                # the suffix decode reads its stable positions (the prompt) while the previous step's
+                # merge drains, and releases the shared pass only after its streaming (that kernel
+                # needs whole SMs: releasing it early measured slower, C5 step 101 -> 140 us)
                 api.rx_decode_cascade_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, sh, q, k, v,
-                                             d[:B], self.k_pool, self.v_pool, o, self._ws)
+                                             d[:B], self.k_pool, self.v_pool, o, self._ws,
+                                             stable_lens=None if _NO_CAS_STABLE else d[3 * B:])
             else:
                 api.rx_decode_append(self.cfg, self._rtt, d[2 * B:3 * B], d[B:2 * B], max_seq, q, k, v, d[:B],
                                      self.k_pool, self.v_pool, o, self._ws, stable_lens=d[3 * B:])

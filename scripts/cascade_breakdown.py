@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--shape", choices=sorted(SHAPES), default="C5")
     ap.add_argument("--steps", type=int, default=32)
     ap.add_argument("--per-request", action="store_true", help="time rx_decode_append instead")
+    ap.add_argument("--no-stable", action="store_true", help="no stable region (wait before any read)")
     a = ap.parse_args()
     (h_q, h_kv, hd), B, L0, P = SHAPES[a.shape]
     dev = "cuda"
@@ -43,7 +44,7 @@ def main():
     kn = torch.randn((a.steps, B, h_kv, hd), device=dev, generator=g).to(torch.bfloat16)
     vn = torch.randn_like(kn)
     o = torch.empty((B, h_q, hd), dtype=torch.bfloat16, device=dev)
-    stable = torch.full((B,), L0 - 1, dtype=torch.int32, device=dev)
+    stable = None if a.no_stable else torch.full((B,), L0 - 1, dtype=torch.int32, device=dev)
     lens = [torch.full((B,), L0 + t, dtype=torch.int32, device=dev) for t in range(a.steps)]
     news = [own[:, L0 - 1 - P + t].contiguous() for t in range(a.steps)]
     wsb = max(rx.rx_decode_cascade_workspace_bytes(cfg, B, Lmax, P), rx.rx_decode_workspace_bytes(cfg, B, Lmax))
