@@ -169,7 +169,10 @@ class Engine:
         # shared-prefix (cascade) decode when the batch shares >= cascade_min_len cached slots
         self.cascade = cascade
         self.cascade_min_len = 256
-        self.cascade_min_batch = 4
+        # G = 1 (no GQA grouping): below 8 requests the per-request decode (one fused launch + merge)
+        # beats the 3-launch cascade chain (2k shared, B = 4: 27.0 vs 33.2 us per step; B = 16:
+        # 52.3 vs 32.5 — profiles/r2_cascade_c4_threshold.txt)
+        self.cascade_min_batch = 8 if wl.shape.h_q == wl.shape.h_kv else 4
         self._shared = 0
         self._ws = None
         self._rtt = None

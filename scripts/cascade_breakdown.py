@@ -18,7 +18,10 @@ import torch
 
 import paper_2312_07104_b200 as rx
 
-SHAPES = {"C5": ((64, 8, 128), 128, 8320, 8192), "C2": ((32, 32, 128), 64, 1700, 1536)}
+SHAPES = {"C5": ((64, 8, 128), 128, 8320, 8192), "C2": ((32, 32, 128), 64, 1700, 1536),
+          # C4 (tree of thought on a 2k root, G = 1): level-1 / level-2 / level-3 decode batches
+          "C4a": ((32, 32, 128), 4, 2160, 2048), "C4b": ((32, 32, 128), 16, 2200, 2048),
+          "C4c": ((32, 32, 128), 64, 2240, 2048)}
 
 
 def main():
