@@ -502,6 +502,24 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch,
 size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, int32_t max_seq_len,
                                          int32_t shared_len);
 
+/* A run of n_steps decode steps in ONE call (Alg. 1's output loop: the
+ * host-side per-step launch cost — argument checks, marshalling — paid once per run).
+ * Step k is exactly rx_decode_cascade_append(cfg, h_batch[k], d_rtt, rtt_stride,
+ * rows, seq_lens, stable, h_max_seq[k], shared_len, h_q[k], h_k_new[k], h_v_new[k],
+ * new_slots, d_k_pool, d_v_pool, num_slots, h_o[k], d_ws, ws_bytes, stream)
+ * (shared_len == 0: rx_decode_append), with its int32 records read from the device
+ * array d_rec at word offset h_rec_off[k]: [new_slots | seq_lens | rows | stable
+ * lens], h_batch[k] words each (the rx_decode_steps staging layout; stable lens
+ * used only when with_stable != 0).  h_*: host arrays of n_steps entries (device
+ * pointers for q / k_new / v_new / o).  Steps are enqueued in order on the stream;
+ * the first failing step's status is returned (earlier steps stay enqueued).
+ * The workspace must fit every step. */
+rx_status rx_decode_run(const rx_attn_cfg* cfg, int32_t n_steps, const int32_t* h_batch, const int32_t* h_max_seq,
+                        int32_t shared_len, int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rec,
+                        const int64_t* h_rec_off, int32_t with_stable, void* const* h_q, void* const* h_k_new,
+                        void* const* h_v_new, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* const* h_o,
+                        void* d_ws, size_t ws_bytes, void* stream);
+
 /* ======================================================================= */
 /*  3. Tensor-parallel output all-gather over peer memory (A9)              */
 /* ======================================================================= */

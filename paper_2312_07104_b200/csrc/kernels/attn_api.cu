@@ -276,6 +276,30 @@ rx_status rx_decode_cascade_append(const rx_attn_cfg* cfg, int32_t batch, int32_
                       nullptr);
 }
 
+rx_status rx_decode_run(const rx_attn_cfg* cfg, int32_t n_steps, const int32_t* h_batch, const int32_t* h_max_seq,
+                        int32_t shared_len, int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rec,
+                        const int64_t* h_rec_off, int32_t with_stable, void* const* h_q, void* const* h_k_new,
+                        void* const* h_v_new, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* const* h_o,
+                        void* d_ws, size_t ws_bytes, void* stream) {
+  if (n_steps < 0 || (n_steps > 0 && (!h_batch || !h_max_seq || !d_rec || !h_rec_off || !h_q || !h_k_new ||
+                                      !h_v_new || !h_o)))
+    return RX_E_INVALID;
+  int32_t total = 0;
+  for (int32_t k = 0; k < n_steps; ++k) {
+    const int32_t B = h_batch[k];
+    if (B < 0 || h_rec_off[k] < 0) return RX_E_INVALID;
+    const int32_t* r = d_rec + h_rec_off[k];   // [new slots | seq_lens | rows | stable lens], B each
+    const rx_status st =
+        cascade_impl(cfg, B, d_rtt, rtt_stride, r + 2 * B, r + B, with_stable ? r + 3 * B : nullptr, h_max_seq[k],
+                     shared_len, h_q[k], h_k_new[k], h_v_new[k], r, d_k_pool, d_v_pool, num_slots, h_o[k], d_ws,
+                     ws_bytes, stream, nullptr);
+    if (st != RX_OK) return st;
+    total += g_last_launches;
+  }
+  g_last_launches = total;
+  return RX_OK;
+}
+
 rx_status rx_decode_append_tp(const rx_attn_cfg* cfg, int32_t batch, int32_t* d_rtt, int64_t rtt_stride,
                               const int32_t* d_rows, const int32_t* d_seq_lens, const int32_t* d_stable_lens,
                               int32_t max_seq_len, int32_t shared_len, const void* d_q, const void* d_k_new,

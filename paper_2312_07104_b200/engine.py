@@ -51,6 +51,8 @@ class OutOfSlots(RuntimeError):
 
 # RX_CASCADE_STABLE=0: cascade decode steps without a stable region (A/B knob)
 _NO_CAS_STABLE = os.environ.get("RX_CASCADE_STABLE", "1") == "0"
+# RX_DECODE_PER_STEP=1: one Python-level library call per decode step instead of rx_decode_run (A/B)
+_PER_STEP_LAUNCH = os.environ.get("RX_DECODE_PER_STEP", "0") == "1"
 
 
 def shard_heads(h_q: int, h_kv: int, rank: int, size: int):
@@ -755,6 +757,9 @@ class Engine:
         # every rank's gathered buffer; one flag barrier ends the run, then the outputs are read
         fused = getattr(self.gather, "fused", False)
         per_call = self.gather is not None and not fused
+        if self.gather is None and not _PER_STEP_LAUNCH:
+            self._decode_run_native(d_all, sn, meta, sh)
+            return
         ev_run = None if per_call else self._tbeg()
         works, nl_run, pending = [], 0, []
         if fused:
@@ -815,6 +820,54 @@ class Engine:
             self._tend(ev_run, "decode", works, nl_run, calls=len(meta))
         if fused:
             self._fused_end_run(pending)
+
+    def _decode_run_native(self, d_all, sn, meta, sh):
+        """The run's steps in ONE library call (rx_decode_run): per-step host cost is the C launch
+        path only (a Python call per step cost ~35-48 us of host time, more than a cascade step's
+        device time on C2 / C4).  Outputs are consecutive views of one buffer."""
+        dev, hd = self.device, self.shape.head_dim
+        ev_run = self._tbeg()
+        n = len(meta)
+        Bs = [int(B) for B, _, _ in meta]
+        o_all = torch.empty((sum(Bs), self.hq, hd), dtype=torch.bfloat16, device=dev)
+        # host-resident inputs (hostio._BlockPrefetcher) hand out a block's ring slot for reuse when
+        # the first call of the NEXT block is taken, i.e. they expect a block's kernels enqueued by
+        # then: cut the run at block boundaries (one library call per block); device banks: one call
+        blk = getattr(self.bank.dec, "block", None)
+        outs, nl, r, k0 = [], 0, 0, 0
+        while k0 < n:
+            qs, ks, vs, os_ = [], [], [], []
+            k1 = k0
+            while k1 < n and (k1 == k0 or blk is None or self._dec_i % blk != 0):
+                q, k, v = self.bank.dec[self._dec_i]
+                self._dec_i += 1
+                qs.append(q)
+                ks.append(k)
+                vs.append(v)
+                os_.append(o_all[r:r + Bs[k1]])
+                r += Bs[k1]
+                k1 += 1
+            api.rx_decode_run(self.cfg, self._rtt, d_all, [int(o0) for _, o0, _ in meta[k0:k1]], Bs[k0:k1],
+                              [int(ms) for _, _, ms in meta[k0:k1]], sh, qs, ks, vs, self.k_pool, self.v_pool, os_,
+                              self._ws, with_stable=not (sh and _NO_CAS_STABLE))
+            nl += api.rx_last_launch_count()
+            outs += os_
+            k0 = k1
+        self.stats["launches"] += nl
+        works = []
+        if sn is not None:
+            # algorithmic bytes (SURVEY §8(d)): distinct pool rows read (K+V) + q + o + slot indices,
+            # computed after the timed region from (slots, running, pos)
+            for B, o0, _ in meta:
+                B, o0 = int(B), int(o0)
+                works.append((self._slots_host, sn[o0 + 2 * B:o0 + 3 * B].astype(np.int64), sn[o0 + B:o0 + 2 * B] - 1))
+        if ev_run is not None:
+            self._tend(ev_run, "decode", works, nl, calls=n)
+        for o, B in zip(outs, Bs):
+            if self.sink is not None:
+                self.sink("decode", o)
+            if self.keep_outputs:
+                self.outputs.append(("decode", o, {"B": B}))
 
     def _fused_end_run(self, pending):
         """End a FusedGather run: the host sink's copies of the previous run are done (a peer may
