@@ -131,14 +131,19 @@ class RadixCache:
         _check(lib.rx_free(self._h, _p32(s), len(s)), "rx_free")
 
     # -------------------------------------------------------------- batched (one C call per step)
-    def rx_match_prefix_batch(self, tokens_concat, offsets):
-        """-> (nodes int64[B], matched int64[B], slots int32 (same layout as tokens_concat))"""
+    def rx_match_prefix_batch(self, tokens_concat, offsets, out=None):
+        """-> (nodes int64[B], matched int64[B], slots int32 (same layout as tokens_concat)); `out`: an
+        int32 buffer of >= len(tokens_concat) entries to write the slots into (reused by the caller:
+        a fresh multi-MB array per call costs page faults)"""
         t = _i32(tokens_concat)
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         B = len(off) - 1
         nodes = np.empty(B, dtype=np.int64)
         matched = np.empty(B, dtype=np.int64)
-        slots = np.empty(max(len(t), 1), dtype=_I32)
+        if out is not None and out.dtype == _I32 and out.flags.c_contiguous and len(out) >= max(len(t), 1):
+            slots = out[:max(len(t), 1)]
+        else:
+            slots = np.empty(max(len(t), 1), dtype=_I32)
         _check(lib.rx_match_prefix_batch(self._h, B, _p32(t), off.ctypes.data_as(P64), nodes.ctypes.data_as(P64),
                                          matched.ctypes.data_as(P64), _p32(slots)), "rx_match_prefix_batch")
         return nodes, matched, slots

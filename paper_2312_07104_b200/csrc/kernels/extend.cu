@@ -706,6 +706,32 @@ static bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t*
   return r == CUDA_SUCCESS;
 }
 
+// Pool tensor maps (3-D (HD, h_kv, S), box (64, 1, 128)) depend only on the pool: encoded once and
+// reused (a decode run issues a cascade step every ~30 us; cuTensorMapEncodeTiled costs ~1-2 us of
+// host time each).  Small per-thread cache keyed by (base, slots, h_kv, HD).
+static bool pool_map(CUtensorMap* m, const void* base, uint64_t slots, int h_kv, int hd) {
+  struct Ent {
+    const void* base;
+    uint64_t slots;
+    int h_kv, hd;
+    CUtensorMap map;
+  };
+  static thread_local Ent cache[4];
+  static thread_local int next = 0;
+  for (const Ent& e : cache)
+    if (e.base == base && e.slots == slots && e.h_kv == h_kv && e.hd == hd) {
+      *m = e.map;
+      return true;
+    }
+  uint64_t dims[3] = {uint64_t(hd), uint64_t(h_kv), slots};
+  uint64_t str[2] = {uint64_t(hd) * 2, uint64_t(h_kv) * hd * 2};
+  uint32_t box[3] = {64, 1, 128};
+  if (!make_map(m, base, 3, dims, str, box)) return false;
+  cache[next] = Ent{base, slots, h_kv, hd, *m};
+  next = (next + 1) & 3;
+  return true;
+}
+
 template <int HD, int G>
 static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t total_new, int batch,
                                    int max_ext, cudaStream_t st) {
@@ -722,19 +748,18 @@ static cudaError_t launch_extend_t(const ExtendParams& p, const void* q, int64_t
     uint32_t box[3] = {64, uint32_t(G), uint32_t(TOK)};
     if (!make_map(&mp.q, q, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
-  {
+  if (!pool_map(&mp.kpool, p.kpool, uint64_t(p.num_slots), p.h_kv, HD) ||
+      !pool_map(&mp.vpool, p.vpool, uint64_t(p.num_slots), p.h_kv, HD))
+    return cudaErrorInvalidValue;
+  if (p.cascade) {   // no new tiles in cascade mode: the new-KV maps are never used
+    mp.knew = mp.kpool;
+    mp.vnew = mp.vpool;
+  } else {
     uint64_t dims[3] = {hd, uint64_t(p.h_kv), N};
     uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
     uint32_t box[3] = {64, 1, kBN};
-    if (!make_map(&mp.knew, p.cascade ? p.kpool : p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
-    if (!make_map(&mp.vnew, p.cascade ? p.vpool : p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
-  }
-  {
-    uint64_t dims[3] = {hd, uint64_t(p.h_kv), uint64_t(p.num_slots)};
-    uint64_t str[2] = {hd * 2, uint64_t(p.h_kv) * hd * 2};
-    uint32_t box[3] = {64, 1, kBN};
-    if (!make_map(&mp.kpool, p.kpool, 3, dims, str, box)) return cudaErrorInvalidValue;
-    if (!make_map(&mp.vpool, p.vpool, 3, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.knew, p.k_new, 3, dims, str, box)) return cudaErrorInvalidValue;
+    if (!make_map(&mp.vnew, p.v_new, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
     cudaError_t e = ensure_smem_attr(extend_kernel<HD, G>, C::SMEM);

@@ -176,6 +176,10 @@ class Engine:
         # 52.3 vs 32.5 — profiles/r2_cascade_c4_threshold.txt)
         self.cascade_min_batch = 8 if wl.shape.h_q == wl.shape.h_kv else 4
         self._shared = 0
+        self._match_cache = {}               # batch key -> (concatenated prompts, offsets)
+        self._match_out = None               # reused slot output buffer of _match
+        self._slot_bufs = []                 # reused host req_to_token mirrors, one per batch of a pass
+        self._slot_buf_i = 0
         self._ws = None
         self._rtt = None
         self._fsm = None                      # compressed FSM of the workload's regex (JSON workload)
@@ -291,13 +295,22 @@ class Engine:
         c = self.cache
         if not rs:
             return
-        toks = np.concatenate([r.tokens[:r.n_prompt] for r in rs])
-        off = np.zeros(len(rs) + 1, dtype=np.int64)
-        off[1:] = np.cumsum([r.n_prompt for r in rs])
-        nodes, matched, sl = c.rx_match_prefix_batch(toks, off)        # one C call per step
+        # the batch's concatenated prompts are the same every pass (cached by request identity), and
+        # the slot output goes into a reused buffer: fresh multi-MB arrays per batch cost page faults
+        key = tuple((r.rid, r.n_prompt) for r in rs)
+        hit = self._match_cache.get(key)
+        if hit is None:
+            toks = np.concatenate([r.tokens[:r.n_prompt] for r in rs])
+            off = np.zeros(len(rs) + 1, dtype=np.int64)
+            off[1:] = np.cumsum([r.n_prompt for r in rs])
+            hit = self._match_cache[key] = (toks, off)
+        toks, off = hit
+        if self._match_out is None or len(self._match_out) < len(toks):
+            self._match_out = np.empty(max(len(toks), 1), dtype=np.int32)
+        nodes, matched, sl = c.rx_match_prefix_batch(toks, off, out=self._match_out)   # one C call
         for b, r in enumerate(rs):
             m = int(matched[b])
-            s = sl[off[b]:off[b] + m]
+            s = sl[off[b]:off[b] + m]          # (a view of the reused buffer: valid until the next match)
             if self.record:
                 self._rec("match", r.rid, m, tuple(int(x) for x in s))
             r.node = int(nodes[b])
@@ -365,7 +378,7 @@ class Engine:
         n_out = np.array([r.n_out for r in rs], dtype=np.int64)
         first = np.array([r.first for r in rs], dtype=np.int64)
         stride = int((n_prompt + n_out).max())
-        slots = np.zeros((B, stride), dtype=np.int32)        # host mirror of this batch's req_to_token rows
+        slots = self._slot_buf(B, stride)                    # host mirror of this batch's req_to_token rows
         prefix = np.array([r.prefix for r in rs], dtype=np.int64)
         for b, r in enumerate(rs):
             slots[b, :r.prefix] = r.slots
@@ -419,6 +432,21 @@ class Engine:
         self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
         return rs
 
+    def _slot_buf(self, B, stride):
+        """A zeroed [B, stride] int32 host mirror for the pass's next batch: buffers are reused
+        across passes (k-th batch of a pass -> k-th buffer; a pass keeps every batch's mirror alive
+        for its decode_bytes records), so steady state writes warm pages instead of faulting fresh
+        ones."""
+        i = self._slot_buf_i
+        self._slot_buf_i += 1
+        if i == len(self._slot_bufs):
+            self._slot_bufs.append(np.zeros(0, dtype=np.int32))
+        if self._slot_bufs[i].size < B * stride:
+            self._slot_bufs[i] = np.zeros(B * stride, dtype=np.int32)
+        out = self._slot_bufs[i][:B * stride].reshape(B, stride)
+        out.fill(0)
+        return out
+
     def _decode_loop_native(self, rs, slots, cur, running, end):
         """Plain decoding through rx_decode_steps: each C call plans launch_chunk iterations of
         Alg. 1's output loop (alloc + evict-retry, table rows, finishes) and writes their device
@@ -433,9 +461,13 @@ class Engine:
         nr = len(running)
         run[:nr] = running
         nodes = np.array([r.node for r in rs], dtype=np.int64)
-        tok_off = np.zeros(B + 1, dtype=np.int64)
-        tok_off[1:] = np.cumsum(end)
-        tokens = np.concatenate([r.tokens[:n] for r, n in zip(rs, end)])
+        key = ("dec",) + tuple((r.rid, int(n)) for r, n in zip(rs, end))
+        hit = self._match_cache.get(key)         # the same every pass: cached (a fresh multi-MB array
+        if hit is None:                          # per batch costs page faults)
+            tok_off = np.zeros(B + 1, dtype=np.int64)
+            tok_off[1:] = np.cumsum(end)
+            hit = self._match_cache[key] = (np.concatenate([r.tokens[:n] for r, n in zip(rs, end)]), tok_off)
+        tokens, tok_off = hit
         collect = self.plan_only and self.collect_calls
         hcat = np.concatenate([r.hashes[:n] for r, n in zip(rs, end)]) if collect else None
         chunk = self.launch_chunk
@@ -976,6 +1008,7 @@ class Engine:
         self.trace = []
         self.outputs = []
         self._ext_i = self._dec_i = 0
+        self._slot_buf_i = 0
         for k in ("prompt_tokens", "cached_prompt_tokens", "extend_tokens", "decode_tokens", "output_tokens",
                   "launches"):
             self.stats[k] = 0
