@@ -551,3 +551,65 @@ def test_concurrent_extends_on_two_streams():
         ref = A.extend(pool, [d["rtt"][b] for b in range(len(d["pre"]))], d["pre"], d["ext"], d["q"].float().numpy(),
                        d["kn"].float().numpy(), d["vn"].float().numpy(), h_q, h_kv, 1 / math.sqrt(hd))
         _cmp(x["o"], ref, "concurrent extend")
+
+
+@pytest.mark.parametrize("h_q,h_kv,hd,shared", [(64, 8, 128, 2048), (32, 32, 128, 0), (8, 2, 64, 300)])
+def test_decode_run_equals_per_step_calls(h_q, h_kv, hd, shared):
+    """rx_decode_run (a run of decode steps in one library call, records read from one staged
+    device array) is bit-identical to the same steps issued one rx_decode_cascade_append /
+    rx_decode_append call at a time: outputs, pool rows and table entries."""
+    rng = np.random.default_rng(h_q + shared)
+    B, steps = 12, 5
+    L0 = shared + 40
+    stride = L0 + 20 + steps + 4
+    S = shared + B * (stride - shared) + 64
+    kp0 = _vals(rng, S, h_kv, KIND_K, hd).cuda()
+    vp0 = _vals(rng, S, h_kv, KIND_V, hd).cuda()
+    rtt0 = np.zeros((B, stride), dtype=np.int32)
+    rtt0[:, :shared] = np.arange(1, shared + 1)
+    own = (shared + 1 + np.arange(B * (stride - shared))).reshape(B, stride - shared).astype(np.int32)
+    lens0 = L0 + rng.integers(0, 20, B)
+    for b in range(B):
+        rtt0[b, shared:lens0[b] - 1] = own[b, :lens0[b] - 1 - shared]
+    cfg = rx.attn_cfg(h_q, h_kv, hd, 1 / math.sqrt(hd))
+    rows = np.arange(B, dtype=np.int32)[::-1].copy()            # batch entry b uses table row B-1-b
+    recs, offs, maxs, qs, ks, vs = [], [], [], [], [], []
+    off = 0
+    for t in range(steps):
+        seq = (lens0[rows] + t).astype(np.int32)
+        new = own[rows, seq - 1 - shared].astype(np.int32)
+        stable = np.full(B, L0 - 1, dtype=np.int32)
+        recs.append(np.concatenate([new, seq, rows, stable]))
+        offs.append(off)
+        off += 4 * B
+        maxs.append(int(seq.max()))
+        qs.append(_vals(rng, B, h_q, KIND_Q, hd).cuda())
+        ks.append(_vals(rng, B, h_kv, KIND_K, hd).cuda())
+        vs.append(_vals(rng, B, h_kv, KIND_V, hd).cuda())
+    rec = torch.from_numpy(np.concatenate(recs)).cuda()
+    need = max(rx.rx_decode_cascade_workspace_bytes(cfg, B, stride, shared) if shared else 0,
+               rx.rx_decode_workspace_bytes(cfg, B, stride))
+    outs = []
+    for mode in ("run", "steps"):
+        kp, vp, rtt = kp0.clone(), vp0.clone(), torch.from_numpy(rtt0).cuda()
+        ws = torch.zeros(need + 1, dtype=torch.uint8, device="cuda")
+        o = [torch.full((B, h_q, hd), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(steps)]
+        if mode == "run":
+            rx.rx_decode_run(cfg, rtt, rec, offs, [B] * steps, maxs, shared, qs, ks, vs, kp, vp, o, ws)
+            assert rx.rx_last_launch_count() >= steps
+        else:
+            for t in range(steps):
+                d = rec[offs[t]:offs[t] + 4 * B]
+                if shared:
+                    rx.rx_decode_cascade_append(cfg, rtt, d[2 * B:3 * B], d[B:2 * B], maxs[t], shared, qs[t], ks[t],
+                                                vs[t], d[:B], kp, vp, o[t], ws, stable_lens=d[3 * B:])
+                else:
+                    rx.rx_decode_append(cfg, rtt, d[2 * B:3 * B], d[B:2 * B], maxs[t], qs[t], ks[t], vs[t], d[:B],
+                                        kp, vp, o[t], ws, stable_lens=d[3 * B:])
+        torch.cuda.synchronize()
+        outs.append((o, kp, vp, rtt))
+    (o1, kp1, vp1, r1), (o2, kp2, vp2, r2) = outs
+    assert torch.equal(kp1, kp2) and torch.equal(vp1, vp2) and torch.equal(r1, r2)
+    for a, b in zip(o1, o2):
+        assert torch.equal(a, b)
+    assert all(torch.isfinite(a.float()).all() for a in o1)
