@@ -513,12 +513,17 @@ size_t rx_decode_cascade_workspace_bytes(const rx_attn_cfg* cfg, int32_t batch, 
  * used only when with_stable != 0).  h_*: host arrays of n_steps entries (device
  * pointers for q / k_new / v_new / o).  Steps are enqueued in order on the stream;
  * the first failing step's status is returned (earlier steps stay enqueued).
- * The workspace must fit every step. */
+ * The workspace must fit every step.
+ * tp_world > 0 (TP with the fused gather, §3 rx_decode_append_tp): step k stores
+ * its rows into every rank's gathered block h_o[k * tp_world + p] ([batch,
+ * tp_h_q_total, head_dim], head offset tp_head_offset) instead of an o; tp_world
+ * = 0: h_o[k] is step k's output [batch, h_q, head_dim]. */
 rx_status rx_decode_run(const rx_attn_cfg* cfg, int32_t n_steps, const int32_t* h_batch, const int32_t* h_max_seq,
                         int32_t shared_len, int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rec,
                         const int64_t* h_rec_off, int32_t with_stable, void* const* h_q, void* const* h_k_new,
                         void* const* h_v_new, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* const* h_o,
-                        void* d_ws, size_t ws_bytes, void* stream);
+                        int32_t tp_world, int32_t tp_h_q_total, int32_t tp_head_offset, void* d_ws,
+                        size_t ws_bytes, void* stream);
 
 /* ======================================================================= */
 /*  3. Tensor-parallel output all-gather over peer memory (A9)              */

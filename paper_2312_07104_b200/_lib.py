@@ -96,7 +96,7 @@ SIGNATURES = {
                                            vp, vp, i64, vp, vp, sz, vp]),
     "rx_decode_cascade_workspace_bytes": (sz, [C.POINTER(AttnCfg), i32, i32, i32]),
     "rx_decode_run": (C.c_int, [C.POINTER(AttnCfg), i32, P32, P32, i32, vp, i64, vp, P64, i32, C.POINTER(vp),
-                                C.POINTER(vp), C.POINTER(vp), vp, vp, i64, C.POINTER(vp), vp, sz, vp]),
+                                C.POINTER(vp), C.POINTER(vp), vp, vp, i64, C.POINTER(vp), i32, i32, i32, vp, sz, vp]),
     "rx_decode_append_tp": (C.c_int, [C.POINTER(AttnCfg), i32, vp, i64, vp, vp, vp, i32, i32, vp, vp, vp, vp,
                                       vp, vp, i64, C.POINTER(TpOut), vp, sz, vp]),
     "rx_last_launch_count": (i32, []),

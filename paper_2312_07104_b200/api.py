@@ -477,15 +477,16 @@ def rx_decode_cascade_append(cfg: AttnCfg, rtt, rows, seq_lens, max_seq_len: int
 
 
 def rx_decode_run(cfg: AttnCfg, rtt, rec, rec_off, batches, max_seqs, shared_len: int, qs, ks, vs, k_pool, v_pool,
-                  outs, ws, with_stable=True, stream=None):
+                  outs, ws, with_stable=True, stream=None, tp=None):
     """A run of decode steps in one C call (include/rx.h rx_decode_run): step k = one
     rx_decode_cascade_append / rx_decode_append over the records rec[rec_off[k]:] ([new slots |
     seq_lens | rows | stable lens], batches[k] int32 words each), q / k_new / v_new / o = qs[k] /
-    ks[k] / vs[k] / outs[k] (CUDA bf16 tensors)."""
+    ks[k] / vs[k] / outs[k] (CUDA bf16 tensors).  tp = (h_q_total, head_offset): fused-gather TP
+    steps, outs[k] = the list of every rank's destination address (int) for step k."""
     import numpy as np
     import torch
     n = len(batches)
-    for name, lst in (("q", qs), ("k_new", ks), ("v_new", vs), ("o", outs)):
+    for name, lst in (("q", qs), ("k_new", ks), ("v_new", vs)) + ((("o", outs),) if tp is None else ()):
         if len(lst) != n:
             raise ValueError(f"rx_decode_run: {name} needs {n} tensors")
         for t in lst:
@@ -493,13 +494,23 @@ def rx_decode_run(cfg: AttnCfg, rtt, rec, rec_off, batches, max_seqs, shared_len
     b = np.ascontiguousarray(batches, dtype=np.int32)
     m = np.ascontiguousarray(max_seqs, dtype=np.int32)
     off = np.ascontiguousarray(rec_off, dtype=np.int64)
-    ptrs = [(C.c_void_p * max(1, n))(*[t.data_ptr() for t in lst]) for lst in (qs, ks, vs, outs)]
+    ptrs = [(C.c_void_p * max(1, n))(*[t.data_ptr() for t in lst]) for lst in (qs, ks, vs)]
+    if tp is None:
+        optr, world, hq_total, head_off = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in outs]), 0, 0, 0
+    else:
+        if len(outs) != n or len({len(o) for o in outs}) > 1:
+            raise ValueError("rx_decode_run: tp outs needs n lists of equal length")
+        world = len(outs[0]) if n else 1
+        flat = [int(a) for o in outs for a in o]
+        optr = (C.c_void_p * max(1, len(flat)))(*flat)
+        hq_total, head_off = int(tp[0]), int(tp[1])
     ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
     st = lib.rx_decode_run(C.byref(cfg), n, b.ctypes.data_as(P32), m.ctypes.data_as(P32), shared_len,
                            _dev(rtt, torch.int32, "rtt"), rtt.shape[1], _dev(rec, torch.int32, "rec"),
                            off.ctypes.data_as(P64), 1 if with_stable else 0, ptrs[0], ptrs[1], ptrs[2],
                            _dev(k_pool, torch.bfloat16, "k_pool"), _dev(v_pool, torch.bfloat16, "v_pool"),
-                           k_pool.shape[0], ptrs[3], _dev(ws, None, "ws"), ws_bytes, _stream(stream))
+                           k_pool.shape[0], optr, world, hq_total, head_off, _dev(ws, None, "ws"), ws_bytes,
+                           _stream(stream))
     _check(st, "rx_decode_run")
 
 

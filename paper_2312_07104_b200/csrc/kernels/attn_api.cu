@@ -280,19 +280,34 @@ rx_status rx_decode_run(const rx_attn_cfg* cfg, int32_t n_steps, const int32_t* 
                         int32_t shared_len, int32_t* d_rtt, int64_t rtt_stride, const int32_t* d_rec,
                         const int64_t* h_rec_off, int32_t with_stable, void* const* h_q, void* const* h_k_new,
                         void* const* h_v_new, void* d_k_pool, void* d_v_pool, int64_t num_slots, void* const* h_o,
-                        void* d_ws, size_t ws_bytes, void* stream) {
+                        int32_t tp_world, int32_t tp_h_q_total, int32_t tp_head_offset, void* d_ws,
+                        size_t ws_bytes, void* stream) {
   if (n_steps < 0 || (n_steps > 0 && (!h_batch || !h_max_seq || !d_rec || !h_rec_off || !h_q || !h_k_new ||
                                       !h_v_new || !h_o)))
     return RX_E_INVALID;
+  if (tp_world < 0 || tp_world > rx::kTpMaxRanks || !cfg ||
+      (tp_world > 0 && (tp_head_offset < 0 || tp_h_q_total < tp_head_offset + cfg->h_q)))
+    return RX_E_INVALID;
+  const int32_t W = tp_world > 0 ? tp_world : 1;
   int32_t total = 0;
   for (int32_t k = 0; k < n_steps; ++k) {
     const int32_t B = h_batch[k];
     if (B < 0 || h_rec_off[k] < 0) return RX_E_INVALID;
     const int32_t* r = d_rec + h_rec_off[k];   // [new slots | seq_lens | rows | stable lens], B each
+    rx::OutSpec os{};
+    if (tp_world > 0) {                        // step k's gathered block on every rank (fused gather)
+      for (int32_t p = 0; p < tp_world; ++p) {
+        if (!h_o[int64_t(k) * W + p]) return RX_E_INVALID;
+        os.ptr[p] = static_cast<__nv_bfloat16*>(h_o[int64_t(k) * W + p]);
+      }
+      os.n = tp_world;
+      os.head_off = tp_head_offset;
+      os.row_stride = int64_t(tp_h_q_total) * cfg->head_dim;
+    }
     const rx_status st =
         cascade_impl(cfg, B, d_rtt, rtt_stride, r + 2 * B, r + B, with_stable ? r + 3 * B : nullptr, h_max_seq[k],
-                     shared_len, h_q[k], h_k_new[k], h_v_new[k], r, d_k_pool, d_v_pool, num_slots, h_o[k], d_ws,
-                     ws_bytes, stream, nullptr);
+                     shared_len, h_q[k], h_k_new[k], h_v_new[k], r, d_k_pool, d_v_pool, num_slots,
+                     tp_world > 0 ? nullptr : h_o[k], d_ws, ws_bytes, stream, tp_world > 0 ? &os : nullptr);
     if (st != RX_OK) return st;
     total += g_last_launches;
   }

@@ -789,8 +789,8 @@ class Engine:
         # every rank's gathered buffer; one flag barrier ends the run, then the outputs are read
         fused = getattr(self.gather, "fused", False)
         per_call = self.gather is not None and not fused
-        if self.gather is None and not _PER_STEP_LAUNCH:
-            self._decode_run_native(d_all, sn, meta, sh)
+        if (self.gather is None or fused) and not _PER_STEP_LAUNCH:
+            self._decode_run_native(d_all, sn, meta, sh, fused)
             return
         ev_run = None if per_call else self._tbeg()
         works, nl_run, pending = [], 0, []
@@ -853,38 +853,64 @@ class Engine:
         if fused:
             self._fused_end_run(pending)
 
-    def _decode_run_native(self, d_all, sn, meta, sh):
-        """The run's steps in ONE library call (rx_decode_run): per-step host cost is the C launch
-        path only (a Python call per step cost ~35-48 us of host time, more than a cascade step's
-        device time on C2 / C4).  Outputs are consecutive views of one buffer."""
+    def _decode_run_native(self, d_all, sn, meta, sh, fused=False):
+        """The run's steps in as few library calls as possible (rx_decode_run): per-step host cost
+        is the C launch path only (a Python call per step cost ~35-48 us of host time, more than a
+        cascade step's device time on C2 / C4).  Outputs are consecutive views of one buffer, or
+        (fused TP gather) of the gather's region on every rank."""
         dev, hd = self.device, self.shape.head_dim
         ev_run = self._tbeg()
         n = len(meta)
         Bs = [int(B) for B, _, _ in meta]
-        o_all = torch.empty((sum(Bs), self.hq, hd), dtype=torch.bfloat16, device=dev)
+        o_all = None if fused else torch.empty((sum(Bs), self.hq, hd), dtype=torch.bfloat16, device=dev)
+        hq_all = self.shape.h_q
         # host-resident inputs (hostio._BlockPrefetcher) hand out a block's ring slot for reuse when
         # the first call of the NEXT block is taken, i.e. they expect a block's kernels enqueued by
-        # then: cut the run at block boundaries (one library call per block); device banks: one call
+        # then: a library call never crosses a block boundary; device banks: one call per run
         blk = getattr(self.bank.dec, "block", None)
-        outs, nl, r, k0 = [], 0, 0, 0
-        while k0 < n:
-            qs, ks, vs, os_ = [], [], [], []
-            k1 = k0
-            while k1 < n and (k1 == k0 or blk is None or self._dec_i % blk != 0):
-                q, k, v = self.bank.dec[self._dec_i]
-                self._dec_i += 1
-                qs.append(q)
-                ks.append(k)
-                vs.append(v)
-                os_.append(o_all[r:r + Bs[k1]])
-                r += Bs[k1]
-                k1 += 1
-            api.rx_decode_run(self.cfg, self._rtt, d_all, [int(o0) for _, o0, _ in meta[k0:k1]], Bs[k0:k1],
-                              [int(ms) for _, _, ms in meta[k0:k1]], sh, qs, ks, vs, self.k_pool, self.v_pool, os_,
-                              self._ws, with_stable=not (sh and _NO_CAS_STABLE))
+        outs, pending, nl, r = [], [], 0, 0
+        chunk = {"k": [], "q": [], "k_": [], "v": [], "o": []}
+
+        def flush():
+            nonlocal nl
+            ks_ = chunk["k"]
+            if not ks_:
+                return
+            api.rx_decode_run(self.cfg, self._rtt, d_all, [int(meta[k][1]) for k in ks_], [Bs[k] for k in ks_],
+                              [int(meta[k][2]) for k in ks_], sh, chunk["q"], chunk["k_"], chunk["v"], self.k_pool,
+                              self.v_pool, chunk["o"], self._ws, with_stable=not (sh and _NO_CAS_STABLE),
+                              tp=(hq_all, int(self.heads_q[0])) if fused else None)
             nl += api.rx_last_launch_count()
-            outs += os_
-            k0 = k1
+            for key in chunk:
+                chunk[key] = []
+
+        if fused:
+            self.gather.begin_run()
+        for k in range(n):
+            B = Bs[k]
+            if blk is not None and self._dec_i % blk == 0:
+                flush()
+            if fused and not self.gather.fits(B, hq_all, hd):   # region full: end the run, start the next
+                flush()
+                self._fused_end_run(pending)
+                pending = []
+                self.gather.begin_run()
+            q, kk, v = self.bank.dec[self._dec_i]
+            self._dec_i += 1
+            if fused:
+                dests, o = self.gather.take(B, hq_all, hd)
+                chunk["o"].append(dests)
+                pending.append((o, B))
+            else:
+                o = o_all[r:r + B]
+                r += B
+                chunk["o"].append(o)
+                outs.append(o)
+            chunk["k"].append(k)
+            chunk["q"].append(q)
+            chunk["k_"].append(kk)
+            chunk["v"].append(v)
+        flush()
         self.stats["launches"] += nl
         works = []
         if sn is not None:
@@ -895,6 +921,9 @@ class Engine:
                 works.append((self._slots_host, sn[o0 + 2 * B:o0 + 3 * B].astype(np.int64), sn[o0 + B:o0 + 2 * B] - 1))
         if ev_run is not None:
             self._tend(ev_run, "decode", works, nl, calls=n)
+        if fused:
+            self._fused_end_run(pending)
+            return
         for o, B in zip(outs, Bs):
             if self.sink is not None:
                 self.sink("decode", o)
