@@ -378,7 +378,7 @@ class Engine:
         n_out = np.array([r.n_out for r in rs], dtype=np.int64)
         first = np.array([r.first for r in rs], dtype=np.int64)
         stride = int((n_prompt + n_out).max())
-        slots = self._slot_buf(B, stride)                    # host mirror of this batch's req_to_token rows
+        slots = self._slot_buf(B, stride, zero=False)        # host mirror of this batch's req_to_token rows
         prefix = np.array([r.prefix for r in rs], dtype=np.int64)
         for b, r in enumerate(rs):
             slots[b, :r.prefix] = r.slots
@@ -389,7 +389,9 @@ class Engine:
         new = self._alloc(int(ext.sum()))
         off = 0
         for b in range(B):
-            slots[b, prefix[b]:prefix[b] + ext[b]] = new[off:off + ext[b]]
+            e = prefix[b] + ext[b]
+            slots[b, prefix[b]:e] = new[off:off + ext[b]]
+            slots[b, e:] = 0                                   # positions the output steps fill later
             off += ext[b]
         self.stats["tree_s"] += time.perf_counter() - t0
         self._slots_host = slots
@@ -432,7 +434,7 @@ class Engine:
         self._rec("sizes", c.rx_evictable_size(), c.rx_total_cached(), c.rx_available())
         return rs
 
-    def _slot_buf(self, B, stride):
+    def _slot_buf(self, B, stride, zero=True):
         """A zeroed [B, stride] int32 host mirror for the pass's next batch: buffers are reused
         across passes (k-th batch of a pass -> k-th buffer; a pass keeps every batch's mirror alive
         for its decode_bytes records), so steady state writes warm pages instead of faulting fresh
@@ -444,7 +446,8 @@ class Engine:
         if self._slot_bufs[i].size < B * stride:
             self._slot_bufs[i] = np.zeros(B * stride, dtype=np.int32)
         out = self._slot_bufs[i][:B * stride].reshape(B, stride)
-        out.fill(0)
+        if zero:
+            out.fill(0)
         return out
 
     def _decode_loop_native(self, rs, slots, cur, running, end):
