@@ -13,7 +13,7 @@ mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 # only this library's kernels (input generation launches thousands of small torch kernels)
 timeout -k 5 2400 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-  -k "regex:decode_kernel|decode_merge_kernel|extend_kernel|extend_store_kernel|store_kv_kernel" \
+  -k "regex:decode_kernel|decode_merge_kernel|cascade_merge_kernel|extend_kernel|extend_store_kernel|store_kv_kernel|tp_allgather_kernel" \
   --log-file gpurun_out/launches_${WL}.csv \
   python bench.py --workload "$WL" --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --configs none > gpurun_out/launches_${WL}.stdout 2>&1
 timeout -k 5 900 $NCU --set full --clock-control none --import-source on -k "regex:${K}" -s ${SKIP} -c ${CNT} \
